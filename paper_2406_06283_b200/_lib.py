@@ -1,0 +1,123 @@
+"""ctypes binding of libhelmgpu.so (include/helmgpu.h).
+
+The shared library is built in-tree (``paper_2406_06283_b200/libhelmgpu.so``,
+see csrc/Makefile).  There is no fallback: if the library is missing or no
+CUDA device is present, the first call raises.
+"""
+
+import ctypes
+import os
+
+from .errors import DeviceError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhelmgpu.so")
+
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_f64p = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+
+
+class HgPrecondDesc(ctypes.Structure):
+    _fields_ = [
+        ("n", ctypes.c_int32),
+        ("nnz", ctypes.c_int64),
+        ("indptr", _i32p),
+        ("indices", _i32p),
+        ("b_data", _f64p),
+        ("dk_data", _f64p),
+        ("n_local", ctypes.c_int32),
+        ("local_n", _i32p),
+        ("local_kl", _i32p),
+        ("local_kv", _i32p),
+        ("local_fstride", _i32p),
+        ("local_bstride", _i32p),
+        ("local_idx_off", _i64p),
+        ("local_idx", _i32p),
+        ("local_fwd_off", _i64p),
+        ("local_fwd_len", ctypes.c_int64),
+        ("local_fwd", _f64p),
+        ("local_bwd_off", _i64p),
+        ("local_bwd_len", ctypes.c_int64),
+        ("local_bwd", _f64p),
+        ("m", ctypes.c_int32),
+        ("n_cblk", ctypes.c_int32),
+        ("cblk_n", _i32p),
+        ("cblk_m", _i32p),
+        ("cblk_idx_off", _i64p),
+        ("cblk_idx", _i32p),
+        ("cblk_z_off", _i64p),
+        ("z_len", ctypes.c_int64),
+        ("z_data", _f64p),
+        ("b0_perm", _i32p),
+        ("b0_kl", ctypes.c_int32),
+        ("b0_ku", ctypes.c_int32),
+        ("b0_lband", _f64p),
+        ("b0_uband", _f64p),
+    ]
+
+
+# name -> (restype, argtypes); every symbol include/helmgpu.h declares
+SIGNATURES = {
+    "hg_abi_version": (ctypes.c_int, []),
+    "hg_last_error": (ctypes.c_char_p, []),
+    "hg_kernel_launches": (ctypes.c_int64, []),
+    "hg_device_sync": (ctypes.c_int, []),
+    "hg_precond_create": (ctypes.c_int, [ctypes.POINTER(HgPrecondDesc), ctypes.POINTER(_vp)]),
+    "hg_precond_destroy": (ctypes.c_int, [_vp]),
+    "hg_precond_device_bytes": (ctypes.c_int64, [_vp]),
+    "hg_precond_apply": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "hg_precond_apply_T": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "hg_precond_apply_coarse": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "hg_precond_spmv": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp]),
+    "hg_local_solve": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp]),
+    "hg_op_create_csr": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, _i32p, _i32p, _f64p, ctypes.POINTER(_vp)]),
+    "hg_op_create_precond": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_vp)]),
+    "hg_op_destroy": (ctypes.c_int, [_vp]),
+    "hg_op_apply": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "hg_gmres": (
+        ctypes.c_int,
+        [_vp, _vp, _vp, _vp, _vp, ctypes.c_double, ctypes.c_int32, _f64p, _i32p, _vp],
+    ),
+    "hg_solve_host": (
+        ctypes.c_int,
+        [_vp, _f64p, _f64p, ctypes.c_double, ctypes.c_int32, _f64p, _i32p, _vp],
+    ),
+}
+
+_LIB = None
+
+
+def load(path=LIB_PATH):
+    """Load the library and bind every exported symbol (raises if absent)."""
+    global _LIB
+    if _LIB is not None and path == LIB_PATH:
+        return _LIB
+    if not os.path.exists(path):
+        raise ImportError(
+            "libhelmgpu.so not built (%s); run `make -C paper_2406_06283_b200/csrc` "
+            "or __graft_entry__.build() — there is no CPU fallback" % path
+        )
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.hg_abi_version() != 1:
+        raise ImportError("libhelmgpu.so ABI mismatch")
+    if path == LIB_PATH:
+        _LIB = lib
+    return lib
+
+
+def check(status, what=""):
+    if status != 0:
+        msg = load().hg_last_error().decode(errors="replace")
+        raise DeviceError("%s failed (status %d): %s" % (what or "helmgpu call", status, msg))
+
+
+def ptr(arr, ctype):
+    """ctypes pointer into a numpy array (None for None / empty)."""
+    if arr is None:
+        return None
+    return arr.ctypes.data_as(ctypes.POINTER(ctype))

@@ -1,0 +1,156 @@
+// Internal device-side data structures and kernel launchers.
+#pragma once
+#include <vector>
+
+#include "hg_common.cuh"
+
+namespace hg {
+
+// Global CSR on device (B and D_k share indptr/indices).
+struct DevCsr {
+  int n = 0;
+  long long nnz = 0;
+  int* indptr = nullptr;
+  int* indices = nullptr;
+  double* data = nullptr;    // B (or the single matrix of a generic op)
+  double* data2 = nullptr;   // D_k (may be null)
+};
+
+struct LocalDesc {   // one fine subdomain block
+  int n, kl, kv, fstride, bstride, pad;
+  long long idx_off;   // into local_idx and the xs scratch
+  long long fwd_off;   // doubles
+  long long bwd_off;   // doubles
+};
+
+struct CblkDesc {    // one coarse (Z) block
+  int n, m, col0, nchunk;
+  long long idx_off;   // into cblk_idx and the zs scratch
+  long long z_off;     // doubles
+  long long part_off;  // into the Z^T r partials
+};
+
+}  // namespace hg
+
+struct HgPrecond {
+  int n = 0;
+  hg::DevCsr A;  // data = B, data2 = D_k
+
+  // one-level part
+  int n_local = 0;
+  int rf = 0, rb = 0;            // register tiles (rows/32) of the two sweeps
+  int max_fstride = 0, max_bstride = 0;
+  hg::LocalDesc* d_local = nullptr;
+  std::vector<hg::LocalDesc> h_local;
+  int* d_local_idx = nullptr;
+  double* d_fwd = nullptr;
+  double* d_bwd = nullptr;
+  long long xs_len = 0;
+  double* d_xs = nullptr;         // per-block local solutions (scratch)
+  // dof -> local contributions (positions in xs), fixed (subdomain) order
+  int* d_lptr = nullptr;
+  long long* d_lent = nullptr;
+
+  // coarse part
+  int m = 0;
+  int n_cblk = 0;
+  hg::CblkDesc* d_cblk = nullptr;
+  std::vector<hg::CblkDesc> h_cblk;
+  int* d_cblk_idx = nullptr;
+  double* d_z = nullptr;
+  long long part_len = 0;
+  double* d_cpart = nullptr;      // Z^T r partial sums
+  int* d_col_blk = nullptr;       // coarse column -> block
+  int2* d_zt_items = nullptr;     // (block, row chunk) work items of Z^T r and Z y
+  int n_zt_items = 0;
+  int* d_b0_perm = nullptr;
+  int b0_kl = 0, b0_ku = 0;
+  double* d_lband = nullptr;
+  double* d_uband = nullptr;
+  double* d_y = nullptr;          // coarse solution (m)
+  long long zs_len = 0;
+  double* d_zs = nullptr;         // per-block Z_b y_b rows (scratch)
+  int* d_cptr = nullptr;
+  long long* d_cent = nullptr;
+
+  double* d_tmp = nullptr;        // n-vector scratch (B u for apply_T)
+  cudaStream_t aux = nullptr;     // coarse chain runs here, forked/joined per apply
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  long long device_bytes = 0;
+  struct HgOp* op_T = nullptr;    // cached operators of hg_solve_host
+  struct HgOp* op_W = nullptr;
+};
+
+namespace hg {
+
+constexpr int VEC_THREADS = 256;
+constexpr int VEC_ROWS = 4;                 // rows per thread
+constexpr int VEC_TILE = VEC_THREADS * VEC_ROWS;
+constexpr int MAX_NV = 1024;                // max vectors in one fused dot
+
+// Block-level partial dots of z against nv vectors W[i] (stride ldw) for the
+// rows this block owns; `zv` holds the thread's VEC_ROWS values of z.
+// Writes partials[blockIdx.x * width + off + i].
+template <int ROWS>
+__device__ __forceinline__ void block_dots(const double (&zv)[ROWS], const int (&rows)[ROWS], int n,
+                                           const double* __restrict__ W, long long ldw, int nv,
+                                           double* __restrict__ partials, int width, int off,
+                                           double* /*unused*/) {
+  __shared__ double s_warp[VEC_THREADS / 32][64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i0 = 0; i0 < nv; i0 += 64) {
+    int cnt = min(64, nv - i0);
+    for (int ii = 0; ii < cnt; ++ii) {
+      const double* wi = W + (long long)(i0 + ii) * ldw;
+      double p = 0.0;
+#pragma unroll
+      for (int k = 0; k < ROWS; ++k)
+        if (rows[k] < n) p = fma(__ldg(wi + rows[k]), zv[k], p);
+      p = warp_sum(p);
+      if (lane == 0) s_warp[warp][ii] = p;
+    }
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < VEC_THREADS / 32; ++w) t += s_warp[w][threadIdx.x];
+      partials[(long long)blockIdx.x * width + off + i0 + threadIdx.x] = t;
+    }
+    __syncthreads();
+  }
+}
+
+
+// ---- launchers (return HG_OK or an error code) ----
+int launch_spmv(const DevCsr& A, const double* vals, const double* x, double* y, cudaStream_t st);
+// y = A x with fused partial dots: self_part[b] = sum x.y over block b;
+// dot_part[b*nv + i] = sum_d W[i][d] * z[d] where z = (dot_with_y ? y : x).
+int launch_spmv_dots(const DevCsr& A, const double* vals, const double* x, double* y, const double* W,
+                     long long ldw, int nv, bool dot_with_y, double* partials, int* nblocks_out,
+                     cudaStream_t st);
+int spmv_dots_nblocks(int n);
+
+int launch_local_solve(HgPrecond* P, const double* r, cudaStream_t st);
+int launch_local_solve_single(HgPrecond* P, int s, const double* r_local, double* x_local, cudaStream_t st);
+int launch_zt(HgPrecond* P, const double* r, cudaStream_t st);
+int launch_coarse_solve(HgPrecond* P, cudaStream_t st);
+int launch_zy(HgPrecond* P, cudaStream_t st);
+// out = coarse + local contributions; optional fused partial dots W[i].out
+int launch_assemble(HgPrecond* P, bool with_coarse, bool with_local, double* out, const double* W,
+                    long long ldw, int nv, double* partials, int* nblocks_out, cudaStream_t st);
+int assemble_nblocks(int n);
+
+// Arnoldi helpers
+int launch_dots(int n, const double* z, const double* W, long long ldw, int nv, double* partials,
+                int* nblocks_out, cudaStream_t st);
+int launch_reduce(const double* partials, int nblocks, int width, double* out, cudaStream_t st);
+// mode 0: w = V c ; 1: w -= V c ; 2: w += V c  (sequential over the nv vectors)
+int launch_axpy_multi(int n, double* w, const double* V, long long ldv, int nv, const double* coef,
+                      int mode, cudaStream_t st);
+int launch_sub(int n, const double* a, const double* b, double* out, cudaStream_t st);  // out = a - b
+int launch_scale2(int n, const double* w, const double* ww, const double* hnorm_dev, double* v_out,
+                  double* wv_out, cudaStream_t st);
+int launch_copy(int n, const double* x, double* y, cudaStream_t st);
+int launch_fill(long long n, double* y, double val, cudaStream_t st);
+
+}  // namespace hg

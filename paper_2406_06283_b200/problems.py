@@ -1,0 +1,215 @@
+"""The BASELINE configurations as reproducible problems, and the setup driver.
+
+Mirrors the pipeline of cli.run_single (cli.py:224-307) up to the solve:
+mesh -> forms -> C_stab -> decomposition -> local GEVPs -> mode selection
+-> coarse space, each phase timed like cli._Timer (cli.py:204-221).  The
+factorisation and the solve are the caller's (factorize / weighted_gmres).
+
+Config mapping (SURVEY.md §8d and the D-items of §0.1):
+  1: n=80,   k=10,  a=1,                       f=1,            4x4,  overlap 2, cap 30
+  2: n=256,  k=40,  a=1,                       f=gauss(0.3,0.6,0.05), 8x8, overlap 2, cap 40
+  3: n=256,  k=40,  a log-uniform[1,100] on 32x32 (seed 1234), f=1, 8x8, overlap 3, cap 40
+  4: n=720,  k=80,  a=1,                       f=N(0,1) nodal (seed 4), 16x16, overlap 2, cap 60  [D7: 716 -> 720]
+  5: n=1024, k=100, a log-uniform[1,10] on 64x64 (seed 5), f=16 x N(0,1) (seeds 5000+c),
+     8x8 / 16x16 / 32x32, overlap 4, cap 60 / 60 / 15                                       [D7, D11]
+q = 1 (fine = coarse subdomains), tau = 2e-5 (1 + C_stab)^2 k^2 (cli.py:70, 271-273),
+caps applied by truncation (D5), rtol 1e-6, x0 = 0, full GMRES.
+"""
+
+import os
+import time
+from concurrent.futures import ProcessPoolExecutor
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse.linalg as spla
+
+from . import coarse as _coarse
+from . import decomp as _decomp
+from . import fem
+from .errors import NearResonanceError
+
+TAU_AUTO_COEFF = 2e-5
+
+
+@dataclass(frozen=True)
+class ProblemConfig:
+    name: str
+    n: int
+    k: float
+    M: int
+    layers: int
+    cap: int
+    q: int = 1
+    coeff: str = "constant"      # or "loguniform"
+    coeff_cells: int = 0
+    coeff_lo: float = 1.0
+    coeff_hi: float = 1.0
+    coeff_seed: int = 0
+    rhs: str = "constant"        # cli rhs spec, or "normal"
+    rhs_seed: int = 0
+    nrhs: int = 1
+    rtol: float = 1e-6
+    maxit: int = 1000
+    cstab: object = "auto"       # "auto" (sparse restatement) or a number
+
+
+CONFIGS = {
+    "1": ProblemConfig("1", n=80, k=10.0, M=4, layers=2, cap=30),
+    "2": ProblemConfig("2", n=256, k=40.0, M=8, layers=2, cap=40, rhs="gaussian:0.3,0.6,0.05"),
+    "3": ProblemConfig("3", n=256, k=40.0, M=8, layers=3, cap=40, coeff="loguniform", coeff_cells=32,
+                       coeff_lo=1.0, coeff_hi=100.0, coeff_seed=1234),
+    "4": ProblemConfig("4", n=720, k=80.0, M=16, layers=2, cap=60, rhs="normal", rhs_seed=4),
+    "5-8": ProblemConfig("5-8", n=1024, k=100.0, M=8, layers=4, cap=60, coeff="loguniform", coeff_cells=64,
+                         coeff_lo=1.0, coeff_hi=10.0, coeff_seed=5, rhs="normal", rhs_seed=5000, nrhs=16),
+    "5-16": ProblemConfig("5-16", n=1024, k=100.0, M=16, layers=4, cap=60, coeff="loguniform", coeff_cells=64,
+                          coeff_lo=1.0, coeff_hi=10.0, coeff_seed=5, rhs="normal", rhs_seed=5000, nrhs=16),
+    "5-32": ProblemConfig("5-32", n=1024, k=100.0, M=32, layers=4, cap=15, coeff="loguniform", coeff_cells=64,
+                          coeff_lo=1.0, coeff_hi=10.0, coeff_seed=5, rhs="normal", rhs_seed=5000, nrhs=16),
+}
+
+
+@dataclass
+class Problem:
+    config: ProblemConfig
+    mesh: object
+    space: object
+    forms: object
+    dec: object
+    rhs: np.ndarray           # (n,) or (n, nrhs)
+    cstab: float
+    tau_target: float
+    results: list
+    selection: object
+    coarse: object
+    times: dict = field(default_factory=dict)
+
+
+def estimate_cstab_sparse(forms, n_near=8):
+    """C_stab = max_j sqrt(lambda_j + k^2) / |lambda_j - k^2| over the (A, S)
+    pencil (analysis.py:159-183), restated with shift-invert Lanczos at k^2.
+
+    The ratio decreases away from k^2 on both sides, so its maximum sits at
+    one of the eigenvalues nearest k^2; ``n_near`` of them are computed and
+    the request is widened until both sides of k^2 are represented (or the
+    lowest eigenvalue is found to lie above k^2)."""
+    k2 = forms.k**2
+    A, S = forms.stiffness.tocsc(), forms.mass.tocsc()
+    n = A.shape[0]
+    if n <= 400:
+        import scipy.linalg
+
+        lams = scipy.linalg.eigh(A.toarray(), S.toarray(), eigvals_only=True)
+    else:
+        kk = min(n_near, n - 2)
+        while True:
+            lams = np.sort(spla.eigsh(A, k=kk, M=S, sigma=k2, which="LM", return_eigenvectors=False))
+            below, above = np.any(lams < k2), np.any(lams > k2)
+            if (below and above) or kk >= n - 2:
+                break
+            if above and not below:
+                lmin = spla.eigsh(A, k=1, M=S, sigma=0.0, which="LM", return_eigenvectors=False)[0]
+                if lmin >= lams.min() - 1e-9 * abs(lams.min()):
+                    break
+            kk = min(2 * kk, n - 2)
+    dist = np.abs(lams - k2)
+    j = int(dist.argmin())
+    if dist[j] <= 1e-10 * max(lams[j], k2):
+        raise NearResonanceError(forms.k, lams[j])
+    return float((np.sqrt(lams + k2) / dist).max())
+
+
+def _coefficient(cfg, mesh):
+    if cfg.coeff == "constant":
+        return fem.coefficient_field(mesh)
+    if cfg.coeff == "loguniform":
+        return fem.loguniform_cell_field(mesh, cfg.coeff_cells, cfg.coeff_lo, cfg.coeff_hi, cfg.coeff_seed)
+    raise ValueError("unknown coefficient %r" % cfg.coeff)
+
+
+def _rhs(cfg, mesh, space):
+    if cfg.rhs == "normal":
+        cols = [np.random.default_rng(cfg.rhs_seed + c).standard_normal(space.n_dofs) for c in range(cfg.nrhs)]
+        return cols[0] if cfg.nrhs == 1 else np.column_stack(cols)
+    return fem.assemble_rhs(mesh, space, fem.rhs_function(cfg.rhs, mesh.h))
+
+
+# ---- GEVP workers (module level so a process pool can pickle them)
+_G = {}
+
+
+def _gevp_worker(i):
+    forms, dec, method, n_wanted = _G["args"]
+    if _G.get("pool"):
+        from threadpoolctl import threadpool_limits
+
+        with threadpool_limits(1):
+            return _gevp_solve(forms, dec, method, n_wanted, i)
+    return _gevp_solve(forms, dec, method, n_wanted, i)
+
+
+def _gevp_solve(forms, dec, method, n_wanted, i):
+    if method == "dense":
+        g = _coarse.assemble_local_gevp(i, forms, dec, validate=False)
+        return _coarse.solve_indefinite_gevp(g)
+    g = _coarse.assemble_local_gevp(i, forms, dec, dense=False)
+    return _coarse.solve_gevp_lanczos(g, n_wanted)
+
+
+def solve_local_gevps(forms, dec, method="auto", n_wanted=None, workers=None):
+    """All coarse-subdomain eigenproblems; 'auto' = dense when every pencil is
+    small (<= 2000 active dofs), Lanczos otherwise.  Runs in a fork pool."""
+    if method == "auto":
+        method = "dense" if max(s.ovdof.size for s in dec.coarse) <= 2000 else "lanczos"
+    _G["args"] = (forms, dec, method, n_wanted)
+    idx = list(range(dec.n_coarse))
+    workers = workers or min(len(idx), os.cpu_count() or 1)
+    try:
+        if workers > 1 and len(idx) > 1:
+            import multiprocessing as mp
+
+            _G["pool"] = True
+            with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("fork")) as ex:
+                return list(ex.map(_gevp_worker, idx, chunksize=max(1, len(idx) // (4 * workers))))
+        return [_gevp_worker(i) for i in idx]
+    finally:
+        _G.clear()
+
+
+def build_problem(cfg, gevp="auto", workers=None, one_level=False, verbose=False):
+    """Run the setup phase of one configuration (timed per phase)."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    times = {}
+
+    def tick(name, t0):
+        times[name] = time.perf_counter() - t0
+        if verbose:
+            print("  setup %-9s %.2f s" % (name, times[name]), flush=True)
+
+    t0 = time.perf_counter()
+    mesh = fem.build_unit_square_mesh(cfg.n)
+    space = fem.build_fe_space(mesh)
+    tick("mesh", t0)
+    t0 = time.perf_counter()
+    forms = fem.assemble_forms(mesh, space, _coefficient(cfg, mesh), cfg.k)
+    rhs = _rhs(cfg, mesh, space)
+    tick("assembly", t0)
+    t0 = time.perf_counter()
+    dec = _decomp.build_two_level(mesh, space, cfg.M, cfg.q, cfg.layers, cfg.layers)
+    tick("decomp", t0)
+    results, selection, coarse, cstab, tau_target = [], None, None, float("nan"), float("nan")
+    if not one_level:
+        t0 = time.perf_counter()
+        cstab = estimate_cstab_sparse(forms) if cfg.cstab == "auto" else float(cfg.cstab)
+        tau_target = TAU_AUTO_COEFF * (1.0 + cstab) ** 2 * cfg.k**2
+        tick("cstab", t0)
+        t0 = time.perf_counter()
+        results = solve_local_gevps(forms, dec, gevp, n_wanted=cfg.cap + 1, workers=workers)
+        tick("gevp", t0)
+        t0 = time.perf_counter()
+        caps = [cfg.cap] * dec.n_coarse
+        selection = _coarse.select_modes(results, tau_target, caps, truncate=True)
+        coarse = _coarse.build_coarse_space(results, selection, dec, forms)
+        tick("coarse", t0)
+    return Problem(cfg, mesh, space, forms, dec, rhs, cstab, tau_target, results, selection, coarse, times)

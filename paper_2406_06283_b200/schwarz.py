@@ -1,0 +1,445 @@
+"""Drop-in GPU replacement of ``helmdd.schwarz.factorize`` and the
+``TwoLevelPreconditioner`` it returns (pkg/src/helmdd/schwarz.py:37-101).
+
+``factorize(forms, dec, coarse=None)`` accepts either this package's setup
+objects or the reference's own (duck-typed: ``forms.helmholtz``,
+``forms.dk``, ``dec.fine_flat()``, ``dec.coarse[i].idof``, ``coarse.Z``,
+``coarse.B0``, ``coarse.column_meta``).  The factorisations happen on the
+host (setup phase); everything the apply touches is uploaded once into a
+device-resident handle of libhelmgpu.so, and every apply runs there.
+
+Inputs to ``apply`` / ``apply_T`` / ``apply_coarse`` may be numpy arrays
+(copied to the device and the result copied back, like the reference's
+return type) or CUDA torch tensors (result stays on the device).  There is
+no CPU path: without the library or a GPU the calls raise.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse as sp
+
+from . import _lib
+from .errors import SingularOperatorError
+from .factor import band_lu, lu_b0, pack_b0, pack_band_records
+
+_DENSE_EIG_LIMIT = 1500
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2406_06283_b200: a CUDA device is required (no CPU fallback)")
+    return torch
+
+
+def _stream():
+    return ctypes.c_void_p(_torch().cuda.current_stream().cuda_stream)
+
+
+def _as_device(v, n):
+    """(device tensor, was_numpy) for a numpy array or CUDA tensor of length n."""
+    torch = _torch()
+    if isinstance(v, torch.Tensor):
+        t = v.detach()
+        if t.device.type != "cuda":
+            t = t.cuda()
+        t = t.to(torch.float64).contiguous()
+        if t.numel() != n:
+            raise ValueError("vector has length %d, operator has %d" % (t.numel(), n))
+        return t.reshape(n), False
+    a = np.ascontiguousarray(np.asarray(v, dtype=np.float64)).reshape(-1)
+    if a.size != n:
+        raise ValueError("vector has length %d, operator has %d" % (a.size, n))
+    return torch.from_numpy(a).cuda(), True
+
+
+def _vp(t):
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class GpuBandLU:
+    """``LocalSolver.lu`` stand-in: ``solve`` runs the device band solve of
+    one block (hg_local_solve); the host factors stay available for tests."""
+
+    def __init__(self, precond, index, host_factor):
+        self._p = precond
+        self._s = index
+        self.host = host_factor
+        self.shape = (host_factor.n, host_factor.n)
+
+    def solve(self, rhs):
+        torch = _torch()
+        t, was_np = _as_device(rhs, self.host.n)
+        out = torch.empty_like(t)
+        _lib.check(
+            _lib.load().hg_local_solve(self._p._handle, self._s, _vp(t), _vp(out), _stream()), "hg_local_solve"
+        )
+        return out.cpu().numpy() if was_np else out
+
+
+class LocalSolver:
+    """Mirror of schwarz.LocalSolver (schwarz.py:26-34); ``min_eig`` and
+    ``spd_flag`` are computed lazily (they only feed reports)."""
+
+    def __init__(self, coarse_index, fine_index, idof, lu, diameter, block):
+        self.coarse_index = coarse_index
+        self.fine_index = fine_index
+        self.idof = idof
+        self.lu = lu
+        self.diameter = diameter
+        self._block = block
+        self._min_eig = None
+
+    @property
+    def min_eig(self):
+        if self._min_eig is None:
+            self._min_eig = _smallest_eigenvalue(self._block) if self.idof.size else np.inf
+        return self._min_eig
+
+    @property
+    def spd_flag(self):
+        return bool(self.min_eig > 0.0)
+
+
+def _smallest_eigenvalue(block):
+    """schwarz.py:134-145."""
+    import scipy.sparse.linalg as spla
+
+    m = block.shape[0]
+    if m <= _DENSE_EIG_LIMIT:
+        return float(scipy.linalg.eigvalsh(block.toarray(), subset_by_index=[0, 0])[0])
+    try:
+        return float(spla.eigsh(block.asfptype(), k=1, which="SA", maxiter=5000, return_eigenvectors=False)[0])
+    except Exception:
+        return float(scipy.linalg.eigvalsh(block.toarray())[0])
+
+
+def _common_pattern(B, Dk):
+    """B and D_k on the union of their patterns (explicit zeros kept), so the
+    device holds one index structure for both (scipy's A - k^2 S may prune an
+    exactly cancelling entry)."""
+    out = []
+    cb, cd = B.tocoo(), Dk.tocoo()
+    rows = np.concatenate([cb.row, cd.row])
+    cols = np.concatenate([cb.col, cd.col])
+    for vals in (
+        np.concatenate([cb.data, np.zeros(cd.nnz)]),
+        np.concatenate([np.zeros(cb.nnz), cd.data]),
+    ):
+        M = sp.coo_matrix((vals, (rows, cols)), shape=B.shape).tocsr()
+        M.sort_indices()
+        out.append(M)
+    if not np.array_equal(out[0].indices, out[1].indices):
+        raise ValueError("B and D_k patterns could not be aligned")
+    return out[0], out[1]
+
+
+def coarse_blocks(coarse, dec):
+    """Per-subdomain dense Z blocks [(index array, n_i x m_i block)] in column order."""
+    if hasattr(coarse, "blocks"):
+        return [(np.asarray(i), np.ascontiguousarray(b)) for i, b in coarse.blocks]
+    Z = sp.csc_matrix(coarse.Z)
+    meta = list(coarse.column_meta)
+    out = []
+    col = 0
+    for i, sub in enumerate(dec.coarse):
+        cols = []
+        while col < len(meta) and meta[col][0] == i:
+            cols.append(col)
+            col += 1
+        idof = np.asarray(sub.idof)
+        if not cols:
+            out.append((idof, np.zeros((idof.size, 0))))
+            continue
+        Zi = Z[:, cols]
+        blk = Zi[idof].toarray()
+        if Zi.nnz != np.count_nonzero(blk):
+            raise ValueError("coarse columns of subdomain %d are not supported on its interior dofs" % i)
+        out.append((idof, blk))
+    if col != len(meta):
+        raise ValueError("coarse.column_meta is not grouped by subdomain in ascending order")
+    return out
+
+
+class TwoLevelPreconditioner:
+    """Device-resident M^{-1} r = Z B0^{-1} Z^T r + sum_s E_s B_s^{-1} R_s r."""
+
+    def __init__(self, forms, dec, coarse=None, b0_lu=None):
+        self.forms = forms
+        self.n = forms.n_dofs if hasattr(forms, "n_dofs") else forms.helmholtz.shape[0]
+        self._handle = None
+        self._keep = []
+        self.Z = None
+        self.b0_piv = None
+        B = sp.csr_matrix(forms.helmholtz)
+        B.sort_indices()
+        Dk = sp.csr_matrix(forms.dk) if getattr(forms, "dk", None) is not None else None
+        if Dk is not None:
+            Dk.sort_indices()
+            if not (np.array_equal(Dk.indptr, B.indptr) and np.array_equal(Dk.indices, B.indices)):
+                B, Dk = _common_pattern(B, Dk)
+        self._B = B
+        self._Dk = Dk
+
+        # ---- local factorisations (schwarz.py:83-85, 104-131)
+        Bc = B.tocsc()
+        self.local_solvers = []
+        factors = []
+        for i, j, sub in dec.fine_flat():
+            idof = np.asarray(sub.idof)
+            block = Bc[idof][:, idof].tocsr() if idof.size else sp.csr_matrix((0, 0))
+            if idof.size:
+                f = band_lu(block, label=(i, j))
+            else:
+                f = band_lu(sp.csr_matrix((0, 0)))
+            factors.append((idof, f))
+            self.local_solvers.append(LocalSolver(i, j, idof, None, getattr(sub, "diameter", np.nan), block))
+
+        # ---- coarse operator (schwarz.py:87-100)
+        cblocks = []
+        lu = piv = None
+        if coarse is not None and coarse.m_total > 0:
+            if b0_lu is None:
+                b0_lu = getattr(coarse, "_b0_lu", None)
+            lu, piv = b0_lu if b0_lu is not None else lu_b0(np.asarray(coarse.B0))
+            self.b0_piv = (lu, piv)
+            self.Z = coarse.Z if not hasattr(coarse, "blocks") else None
+            self._coarse = coarse
+            cblocks = coarse_blocks(coarse, dec)
+        self._upload(B, Dk, factors, cblocks, lu, piv)
+        for s, ls in enumerate(self.local_solvers):
+            ls.lu = GpuBandLU(self, s, factors[s][1])
+
+    # ------------------------------------------------------------------ upload
+    def _upload(self, B, Dk, factors, cblocks, lu, piv):
+        keep = self._keep
+        lib = _lib.load()
+        _torch()  # CUDA context present before the first allocation
+        d = _lib.HgPrecondDesc()
+        i32, i64, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+
+        def arr(a, dtype, ctype):
+            a = np.ascontiguousarray(a, dtype=dtype)
+            keep.append(a)
+            return _lib.ptr(a, ctype)
+
+        d.n = self.n
+        d.nnz = B.nnz
+        d.indptr = arr(B.indptr, np.int32, i32)
+        d.indices = arr(B.indices, np.int32, i32)
+        d.b_data = arr(B.data, np.float64, f64)
+        d.dk_data = arr(Dk.data, np.float64, f64) if Dk is not None else None
+
+        ns, kls, kvs, fss, bss = [], [], [], [], []
+        idx_off = [0]
+        fwd_parts, bwd_parts, foff, boff = [], [], [], []
+        fpos = bpos = 0
+        for idof, f in factors:
+            fw, bw, fs, bs = pack_band_records(f)
+            ns.append(f.n)
+            kls.append(f.kl)
+            kvs.append(f.kv)
+            fss.append(fs)
+            bss.append(bs)
+            idx_off.append(idx_off[-1] + idof.size)
+            foff.append(fpos)
+            boff.append(bpos)
+            fwd_parts.append(fw.ravel())
+            bwd_parts.append(bw.ravel())
+            fpos += fw.size
+            bpos += bw.size
+        fwd = np.concatenate(fwd_parts) if fwd_parts else np.zeros(0)
+        bwd = np.concatenate(bwd_parts) if bwd_parts else np.zeros(0)
+        d.n_local = len(factors)
+        d.local_n = arr(ns, np.int32, i32)
+        d.local_kl = arr(kls, np.int32, i32)
+        d.local_kv = arr(kvs, np.int32, i32)
+        d.local_fstride = arr(fss, np.int32, i32)
+        d.local_bstride = arr(bss, np.int32, i32)
+        d.local_idx_off = arr(idx_off, np.int64, i64)
+        d.local_idx = arr(np.concatenate([i for i, _ in factors]) if factors else np.zeros(0), np.int32, i32)
+        d.local_fwd_off = arr(foff, np.int64, i64)
+        d.local_fwd_len = fwd.size
+        d.local_fwd = arr(fwd, np.float64, f64)
+        d.local_bwd_off = arr(boff, np.int64, i64)
+        d.local_bwd_len = bwd.size
+        d.local_bwd = arr(bwd, np.float64, f64)
+
+        m = sum(b.shape[1] for _, b in cblocks)
+        d.m = m
+        if m:
+            perm, kl, ku, lband, uband = pack_b0(lu, piv)
+            self.b0_band = (kl, ku)
+            d.n_cblk = len(cblocks)
+            d.cblk_n = arr([i.size for i, _ in cblocks], np.int32, i32)
+            d.cblk_m = arr([b.shape[1] for _, b in cblocks], np.int32, i32)
+            d.cblk_idx_off = arr(np.concatenate([[0], np.cumsum([i.size for i, _ in cblocks])]), np.int64, i64)
+            d.cblk_idx = arr(np.concatenate([i for i, _ in cblocks]), np.int32, i32)
+            zsizes = [b.size for _, b in cblocks]
+            d.cblk_z_off = arr(np.concatenate([[0], np.cumsum(zsizes)[:-1]]), np.int64, i64)
+            z = np.concatenate([b.ravel() for _, b in cblocks])
+            d.z_len = z.size
+            d.z_data = arr(z, np.float64, f64)
+            d.b0_perm = arr(perm, np.int32, i32)
+            d.b0_kl = kl
+            d.b0_ku = ku
+            d.b0_lband = arr(lband if kl else np.zeros(1), np.float64, f64)
+            d.b0_uband = arr(uband, np.float64, f64)
+        h = ctypes.c_void_p()
+        _lib.check(lib.hg_precond_create(ctypes.byref(d), ctypes.byref(h)), "hg_precond_create")
+        self._handle = h
+        self._keep = []  # host copies no longer needed
+        self.local_bands = [(f.kl, f.kv) for _, f in factors]
+
+    # ------------------------------------------------------------------ API
+    @property
+    def has_coarse(self):
+        return self.b0_piv is not None
+
+    @property
+    def device_bytes(self):
+        return int(_lib.load().hg_precond_device_bytes(self._handle))
+
+    def _run(self, fn, v):
+        torch = _torch()
+        t, was_np = _as_device(v, self.n)
+        out = torch.empty_like(t)
+        _lib.check(getattr(_lib.load(), fn)(self._handle, _vp(t), _vp(out), _stream()), fn)
+        return out.cpu().numpy() if was_np else out
+
+    def apply(self, r):
+        """M^{-1} r (schwarz.py:51-61); returns a new array."""
+        return self._run("hg_precond_apply", r)
+
+    def apply_T(self, u):
+        """T u = M^{-1} B u (schwarz.py:63-65)."""
+        return self._run("hg_precond_apply_T", u)
+
+    def apply_coarse(self, r):
+        """Z B0^{-1} Z^T r (schwarz.py:67-71)."""
+        return self._run("hg_precond_apply_coarse", r)
+
+    def spmv(self, x, which="B"):
+        torch = _torch()
+        t, was_np = _as_device(x, self.n)
+        out = torch.empty_like(t)
+        _lib.check(
+            _lib.load().hg_precond_spmv(self._handle, 0 if which == "B" else 1, _vp(t), _vp(out), _stream()),
+            "hg_precond_spmv",
+        )
+        return out.cpu().numpy() if was_np else out
+
+    def as_operator(self, kind="T"):
+        """Device operator for weighted_gmres: "T" = M^{-1} B (cli.py:298),
+        "M" = M^{-1}, "B" = B, "Dk" = D_k."""
+        return DeviceOperator(self, {"M": 0, "T": 1, "B": 2, "Dk": 3}[kind])
+
+    def solve_host(self, f, rtol=1e-6, maxit=200):
+        """End-to-end solve through the C ABI with host buffers (hg_solve_host):
+        rhs_p = M^{-1} f, x = GMRES(M^{-1} B, rhs_p, weight D_k)."""
+        from .wgmres import GmresReport
+
+        f = np.ascontiguousarray(np.asarray(f, dtype=np.float64))
+        x = np.empty_like(f)
+        maxit = int(min(maxit, self.n))
+        hist = np.zeros(maxit + 1)
+        info = np.zeros(4, dtype=np.int32)
+        _lib.check(
+            _lib.load().hg_solve_host(
+                self._handle, _lib.ptr(f, ctypes.c_double), _lib.ptr(x, ctypes.c_double), float(rtol), maxit,
+                _lib.ptr(hist, ctypes.c_double), _lib.ptr(info, ctypes.c_int32), _stream(),
+            ),
+            "hg_solve_host",
+        )
+        it = int(info[0])
+        rep = GmresReport(iterations=it, residual_history=hist[: it + 1].copy(), converged=bool(info[1]),
+                          breakdown=bool(info[2]))
+        rep.reorth_passes = int(info[3])
+        return x, rep
+
+    def close(self):
+        if self._handle is not None:
+            _lib.load().hg_precond_destroy(self._handle)
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceOperator:
+    """A linear operator that lives on the device (an HgOp)."""
+
+    def __init__(self, precond, mode):
+        self.precond = precond
+        self.mode = mode
+        self.n = precond.n
+        h = ctypes.c_void_p()
+        _lib.check(_lib.load().hg_op_create_precond(precond._handle, mode, ctypes.byref(h)), "hg_op_create_precond")
+        self._handle = h
+
+    def __call__(self, v):
+        torch = _torch()
+        t, was_np = _as_device(v, self.n)
+        out = torch.empty_like(t)
+        _lib.check(_lib.load().hg_op_apply(self._handle, _vp(t), _vp(out), _stream()), "hg_op_apply")
+        return out.cpu().numpy() if was_np else out
+
+    def __del__(self):
+        try:
+            if self._handle is not None:
+                _lib.load().hg_op_destroy(self._handle)
+                self._handle = None
+        except Exception:
+            pass
+
+
+class CsrOperator:
+    """A host sparse/dense matrix uploaded once as a device CSR operator."""
+
+    def __init__(self, mat):
+        A = sp.csr_matrix(mat, dtype=np.float64)
+        A.sort_indices()
+        self.n = A.shape[0]
+        if A.shape[0] != A.shape[1]:
+            raise ValueError("operator must be square")
+        ip = np.ascontiguousarray(A.indptr, dtype=np.int32)
+        ix = np.ascontiguousarray(A.indices, dtype=np.int32)
+        dv = np.ascontiguousarray(A.data, dtype=np.float64)
+        h = ctypes.c_void_p()
+        _torch()
+        _lib.check(
+            _lib.load().hg_op_create_csr(
+                self.n, A.nnz, _lib.ptr(ip, ctypes.c_int32), _lib.ptr(ix, ctypes.c_int32),
+                _lib.ptr(dv, ctypes.c_double), ctypes.byref(h),
+            ),
+            "hg_op_create_csr",
+        )
+        self._handle = h
+        self.matrix = A
+
+    def __call__(self, v):
+        torch = _torch()
+        t, was_np = _as_device(v, self.n)
+        out = torch.empty_like(t)
+        _lib.check(_lib.load().hg_op_apply(self._handle, _vp(t), _vp(out), _stream()), "hg_op_apply")
+        return out.cpu().numpy() if was_np else out
+
+    def __del__(self):
+        try:
+            if self._handle is not None:
+                _lib.load().hg_op_destroy(self._handle)
+                self._handle = None
+        except Exception:
+            pass
+
+
+def factorize(forms, dec, coarse=None):
+    """GPU ``factorize`` (schwarz.py:74-101): host factorisations + upload."""
+    return TwoLevelPreconditioner(forms, dec, coarse)

@@ -1,0 +1,43 @@
+"""The C-ABI library loads on a CPU-only host and exports every symbol
+include/helmgpu.h declares (no compute calls)."""
+
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    text = open(os.path.join(ROOT, "include", "helmgpu.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(hg_[a-z_A-Z0-9]+)\s*\(", text)))
+
+
+def test_header_declares_the_abi():
+    names = _declared()
+    for must in ("hg_precond_create", "hg_precond_apply", "hg_gmres", "hg_solve_host", "hg_last_error"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2406_06283_b200 import _lib
+
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("libhelmgpu.so not built")
+    lib = _lib.load()
+    for name in _declared():
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, name
+    assert lib.hg_abi_version() == 1
+    assert lib.hg_last_error() == b""
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2406_06283_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle\b", src, flags=re.M), f

@@ -1,0 +1,70 @@
+"""Band LU records: the packed layout, interpreted with the kernel's exact
+semantics, reproduces LAPACK dgbtrs and a dense solve (CPU)."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import paper_2406_06283_b200 as hg
+from paper_2406_06283_b200 import factor
+from _helpers import emulate_band_records
+
+
+def _banded(rng, n, w, weak_diag=False):
+    A = np.zeros((n, n))
+    for i in range(n):
+        for j in range(max(0, i - w), min(n, i + w + 1)):
+            A[i, j] = rng.standard_normal()
+    if weak_diag:
+        A[np.arange(n), np.arange(n)] *= 1e-3  # forces row interchanges
+    return sp.csr_matrix(A)
+
+
+@pytest.mark.parametrize("n,w,weak", [(7, 2, False), (50, 5, True), (97, 24, True), (130, 40, False)])
+def test_records_match_dgbtrs(n, w, weak):
+    rng = np.random.default_rng(n)
+    A = _banded(rng, n, w, weak)
+    f = factor.band_lu(A)
+    assert f.kl == w and f.ku == w
+    if weak:
+        assert np.any(f.piv != np.arange(n))
+    fwd, bwd, fs, bs = factor.pack_band_records(f)
+    assert fs % 2 == 0 and bs % 2 == 0 and fs >= f.kl + 1 and bs >= f.kv + 1
+    b = rng.standard_normal(n)
+    x_rec = emulate_band_records(fwd, bwd, n, f.kl, f.kv, b)
+    x_lap = f.solve(b)
+    x_dense = np.linalg.solve(A.toarray(), b)
+    assert np.abs(x_rec - x_lap).max() <= 1e-12 * np.abs(x_lap).max()
+    assert np.abs(x_rec - x_dense).max() <= 1e-9 * np.abs(x_dense).max()
+
+
+def test_helmholtz_blocks_match_superlu(golden):
+    P = hg.build_problem("1", workers=1, one_level=True)
+    B = P.forms.helmholtz.tocsc()
+    import scipy.sparse.linalg as spla
+
+    for i, j, sub in list(P.dec.fine_flat())[:4]:
+        blk = B[sub.idof][:, sub.idof]
+        f = factor.band_lu(blk, label=(i, j))
+        fwd, bwd, _, _ = factor.pack_band_records(f)
+        r = np.random.default_rng(i).standard_normal(sub.idof.size)
+        x = emulate_band_records(fwd, bwd, f.n, f.kl, f.kv, r)
+        ref = spla.splu(blk.tocsc()).solve(r)
+        assert np.abs(x - ref).max() <= 1e-11 * np.abs(ref).max()
+
+
+def test_singular_block_is_named():
+    # k^2 exactly on a Dirichlet eigenvalue of the first fine block (test_schwarz.py:164-180)
+    import scipy.linalg
+
+    mesh = hg.build_unit_square_mesh(8)
+    space = hg.build_fe_space(mesh)
+    probe = hg.assemble_forms(mesh, space, hg.coefficient_field(mesh), 1.0)
+    dec = hg.build_two_level(mesh, space, 2, 2)
+    idof = dec.fine[0][0].idof
+    mu = scipy.linalg.eigh(probe.stiffness[idof][:, idof].toarray(), probe.mass[idof][:, idof].toarray(),
+                           eigvals_only=True)[0]
+    forms = hg.assemble_forms(mesh, space, hg.coefficient_field(mesh), np.sqrt(mu))
+    blk = forms.helmholtz.tocsc()[idof][:, idof]
+    with pytest.raises(hg.SingularOperatorError, match=r"\(0, 0\)"):
+        factor.band_lu(blk, label=(0, 0))
