@@ -141,6 +141,15 @@ int hg_precond_spmv(HgPrecond* p, int which, const double* x, double* y, void* s
  * length local_n[s] (LocalSolver.lu.solve). */
 int hg_local_solve(HgPrecond* p, int s, const double* r_local, double* x_local, void* stream);
 
+/* Stage timing of the apply (no reference analogue; measurement hook used by
+ * bench.py): runs `iters` applies with the stages serialised on `stream`
+ * and CUDA events between them; stage_ms (host, HG_NSTAGES doubles) gets the
+ * mean device time per stage: {Z^T r, B0 solve, Z y, local band solves,
+ * assembly}. */
+#define HG_NSTAGES 5
+int hg_precond_profile(HgPrecond* p, const double* r, double* out, int32_t iters, double* stage_ms,
+                       void* stream);
+
 /* ---- operators for GMRES ---- */
 /* General square CSR operator uploaded from host arrays. */
 int hg_op_create_csr(int32_t n, int64_t nnz, const int32_t* indptr, const int32_t* indices,

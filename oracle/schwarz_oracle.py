@@ -16,7 +16,7 @@ import scipy.sparse.linalg as spla
 
 
 class OraclePreconditioner:
-    def __init__(self, forms, dec, coarse=None):
+    def __init__(self, forms, dec, coarse=None, b0_lu=None):
         self.B = sp.csr_matrix(forms.helmholtz)
         self.n = self.B.shape[0]
         Bc = self.B.tocsc()
@@ -30,7 +30,8 @@ class OraclePreconditioner:
         self.lu = None
         if coarse is not None and coarse.m_total > 0:
             self.Z = sp.csc_matrix(coarse.Z)
-            self.lu = scipy.linalg.lu_factor(np.asarray(coarse.B0))
+            # b0_lu: an existing lu_factor(B0) (identical call) to skip recomputing it
+            self.lu = b0_lu if b0_lu is not None else scipy.linalg.lu_factor(np.asarray(coarse.B0))
 
     def apply(self, r):
         r = np.asarray(r, dtype=float)

@@ -35,6 +35,7 @@ import scipy.sparse.linalg as spla
 
 from .errors import EigensolveError, ModeCapError, SingularOperatorError
 from .fem import local_forms_sparse
+from .factor import submatrix
 
 _GAMMA_ATTEMPTS = 40
 _PIVOT_RTOL = 1e-12
@@ -96,6 +97,7 @@ class CoarseSpace:
     column_meta: list
     removed: list
     _Z: object = field(default=None, repr=False)
+    _b0_lu: object = field(default=None, repr=False)
 
     @property
     def m_total(self):
@@ -419,15 +421,16 @@ def build_coarse_space(results, selection, dec, forms, dense_rank_filter_max=300
             continue
         ia, za = blocks[a]
         ib, zb = blocks[b]
-        Bab = B[ia][:, ib]
+        Bab = submatrix(B, ia, ib)
         B0[offs[a]:offs[a + 1], offs[b]:offs[b + 1]] = za.T @ (Bab @ zb)
     B0 = 0.5 * (B0 + B0.T)
 
     keep = list(range(m_total))
     removed = []
     certified = False
+    b0_lu = None
     if m_total > dense_rank_filter_max:
-        certified, _ = _sym_extreme_certificate(B0, _PIVOT_RTOL)
+        certified, b0_lu = _sym_extreme_certificate(B0, _PIVOT_RTOL)
     if not certified:
         while keep:
             drop = _near_null_columns(B0[np.ix_(keep, keep)])
@@ -450,7 +453,10 @@ def build_coarse_space(results, selection, dec, forms, dense_rank_filter_max=300
         blocks = new_blocks
         meta = [meta[i] for i in keep]
         counts = [b.shape[1] for _, b in blocks]
-    return CoarseSpace(blocks, n, counts, selection.tau, selection.theta, B0, meta, removed)
+    cs = CoarseSpace(blocks, n, counts, selection.tau, selection.theta, B0, meta, removed)
+    if b0_lu is not None and not removed:
+        cs._b0_lu = b0_lu  # getrf of B0 already computed by the certificate; factorize reuses it
+    return cs
 
 
 def spectrum_rows(results, selection):

@@ -405,6 +405,45 @@ int hg_precond_apply_coarse(HgPrecond* P, const double* r, double* out, void* st
   return launch_assemble(P, true, false, out, nullptr, 0, 0, nullptr, nullptr, st);
 }
 
+int hg_precond_profile(HgPrecond* P, const double* r, double* out, int32_t iters, double* stage_ms,
+                       void* stream) {
+  if (!P || !r || !out || !stage_ms || iters <= 0) {
+    set_error("hg_precond_profile: bad argument");
+    return HG_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t ev[HG_NSTAGES + 1];
+  for (auto& e : ev) HG_CUDA_TRY(cudaEventCreate(&e));
+  double acc[HG_NSTAGES] = {0, 0, 0, 0, 0};
+  int status = HG_OK;
+  for (int it = 0; it < iters && status == HG_OK; ++it) {
+    cudaEventRecord(ev[0], st);
+    if ((status = launch_zt(P, r, st)) != HG_OK) break;
+    cudaEventRecord(ev[1], st);
+    if ((status = launch_coarse_solve(P, st)) != HG_OK) break;
+    cudaEventRecord(ev[2], st);
+    if ((status = launch_zy(P, st)) != HG_OK) break;
+    cudaEventRecord(ev[3], st);
+    if ((status = launch_local_solve(P, r, st)) != HG_OK) break;
+    cudaEventRecord(ev[4], st);
+    if ((status = launch_assemble(P, true, true, out, nullptr, 0, 0, nullptr, nullptr, st)) != HG_OK) break;
+    cudaEventRecord(ev[5], st);
+    if (cudaEventSynchronize(ev[5]) != cudaSuccess) {
+      set_error("hg_precond_profile: event sync failed");
+      status = HG_ERR_CUDA;
+      break;
+    }
+    for (int s = 0; s < HG_NSTAGES; ++s) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[s], ev[s + 1]);
+      acc[s] += ms;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int s = 0; s < HG_NSTAGES; ++s) stage_ms[s] = acc[s] / iters;
+  return status;
+}
+
 int hg_precond_spmv(HgPrecond* P, int which, const double* x, double* y, void* stream) {
   if (!P || !x || !y || (which != 0 && which != 1)) {
     set_error("hg_precond_spmv: bad argument");

@@ -23,7 +23,7 @@ import scipy.sparse as sp
 
 from . import _lib
 from .errors import SingularOperatorError
-from .factor import band_lu, lu_b0, pack_b0, pack_band_records
+from .factor import band_lu, lu_b0, pack_b0, pack_band_records, submatrix
 
 _DENSE_EIG_LIMIT = 1500
 
@@ -186,12 +186,11 @@ class TwoLevelPreconditioner:
         self._Dk = Dk
 
         # ---- local factorisations (schwarz.py:83-85, 104-131)
-        Bc = B.tocsc()
         self.local_solvers = []
         factors = []
         for i, j, sub in dec.fine_flat():
             idof = np.asarray(sub.idof)
-            block = Bc[idof][:, idof].tocsr() if idof.size else sp.csr_matrix((0, 0))
+            block = submatrix(B, idof, idof) if idof.size else sp.csr_matrix((0, 0))
             if idof.size:
                 f = band_lu(block, label=(i, j))
             else:
@@ -205,7 +204,7 @@ class TwoLevelPreconditioner:
         if coarse is not None and coarse.m_total > 0:
             if b0_lu is None:
                 b0_lu = getattr(coarse, "_b0_lu", None)
-            lu, piv = b0_lu if b0_lu is not None else lu_b0(np.asarray(coarse.B0))
+            lu, piv = lu_b0(np.asarray(coarse.B0), b0_lu)
             self.b0_piv = (lu, piv)
             self.Z = coarse.Z if not hasattr(coarse, "blocks") else None
             self._coarse = coarse
@@ -271,9 +270,14 @@ class TwoLevelPreconditioner:
 
         m = sum(b.shape[1] for _, b in cblocks)
         d.m = m
+        self.m = m
+        self.local_sizes = ns
+        self.cblock_shapes = [b.shape for _, b in cblocks]
+        self.b0_bytes = 0
         if m:
             perm, kl, ku, lband, uband = pack_b0(lu, piv)
             self.b0_band = (kl, ku)
+            self.b0_bytes = 8 * m * (kl + ku + 1) + 4 * m
             d.n_cblk = len(cblocks)
             d.cblk_n = arr([i.size for i, _ in cblocks], np.int32, i32)
             d.cblk_m = arr([b.shape[1] for _, b in cblocks], np.int32, i32)
@@ -332,6 +336,21 @@ class TwoLevelPreconditioner:
             "hg_precond_spmv",
         )
         return out.cpu().numpy() if was_np else out
+
+    STAGES = ("zt", "b0_solve", "zy", "local", "assemble")
+
+    def profile(self, r, iters=10):
+        """Mean device ms per apply stage, stages serialised (hg_precond_profile)."""
+        torch = _torch()
+        t, _ = _as_device(r, self.n)
+        out = torch.empty_like(t)
+        ms = np.zeros(len(self.STAGES))
+        _lib.check(
+            _lib.load().hg_precond_profile(self._handle, _vp(t), _vp(out), int(iters),
+                                           _lib.ptr(ms, ctypes.c_double), _stream()),
+            "hg_precond_profile",
+        )
+        return dict(zip(self.STAGES, ms.tolist()))
 
     def as_operator(self, kind="T"):
         """Device operator for weighted_gmres: "T" = M^{-1} B (cli.py:298),
