@@ -72,9 +72,9 @@ typedef struct {
    * .. local_idx_off[s+1]) (ascending).  Its pivoted band LU (LAPACK dgbtrf
    * semantics, lower bandwidth kl, U bandwidth kv = kl + ku) is packed as two
    * record streams of fixed stride per block:
-   *   forward  record j (j = 0..n_s-1):  [ipiv_j, l_{j+1,j}, ..., l_{j+kl,j}, pad]
+   *   forward  record j (j = 0..n_s-1):  [l_{j+1,j}, ..., l_{j+kl,j}, ipiv_j, pad]
    *   backward record r (r = 0..n_s-1, j = n_s-1-r):
-   *                                      [1/u_jj, u_{j-1,j}, ..., u_{j-kv,j}, pad]
+   *                                      [u_{j-1,j}, ..., u_{j-kv,j}, 1/u_jj, pad]
    * with local_fstride / local_bstride doubles per record (even), zeros past
    * the end of the block, ipiv stored as an exact double (0-based). */
   int32_t n_local;

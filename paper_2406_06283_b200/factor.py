@@ -10,8 +10,8 @@
   outside a band; ``pack_b0`` measures that band and stores only it.
 
 Record layout consumed by the band-solve kernel (include/helmgpu.h):
-  forward  record j  = [ipiv_j, l_{j+1,j}, ..., l_{j+kl,j}]   (stride even)
-  backward record r  = [1/u_jj, u_{j-1,j}, ..., u_{j-kv,j}],  j = n-1-r
+  forward  record j  = [l_{j+1,j}, ..., l_{j+kl,j}, ipiv_j]   (stride even)
+  backward record r  = [u_{j-1,j}, ..., u_{j-kv,j}, 1/u_jj],  j = n-1-r
 """
 
 from dataclasses import dataclass
@@ -109,28 +109,33 @@ def _even(x):
     return x + (x & 1)
 
 
+MIN_RECORD_WIDTH = 3  # the kernel's replicated front reads the first 3 multipliers
+
+
 def pack_band_records(f):
-    """(fwd records, bwd records, fstride, bstride) for one BandLU."""
+    """(fwd records, bwd records, fstride, bstride, kl_rec, kv_rec) for one
+    BandLU; widths below MIN_RECORD_WIDTH are zero padded (kl_rec, kv_rec)."""
     n, kl, kv = f.n, f.kl, f.kv
-    fs, bs = _even(kl + 1), _even(kv + 1)
+    klp, kvp = max(kl, MIN_RECORD_WIDTH), max(kv, MIN_RECORD_WIDTH)
+    fs, bs = _even(klp + 1), _even(kvp + 1)
     fwd = np.zeros((n, fs))
     bwd = np.zeros((n, bs))
     if n == 0:
-        return fwd, bwd, fs, bs
-    fwd[:, 0] = f.piv
+        return fwd, bwd, fs, bs, klp, kvp
+    fwd[:, klp] = f.piv
     if kl:
         L = f.lub[kv + 1 : kv + 1 + kl, :].T.copy()        # L[j, t-1] = l_{j+t, j}
         j = np.arange(n)[:, None]
         t = np.arange(1, kl + 1)[None, :]
         L[j + t >= n] = 0.0
-        fwd[:, 1 : kl + 1] = L
+        fwd[:, 0:kl] = L
     jj = n - 1 - np.arange(n)                                # backward order
-    bwd[:, 0] = 1.0 / f.lub[kv, jj]
+    bwd[:, kvp] = 1.0 / f.lub[kv, jj]
     if kv:
         U = f.lub[kv - np.arange(1, kv + 1)[:, None], jj[None, :]].T.copy()  # U[r, t-1] = u_{j-t, j}
         U[(jj[:, None] - np.arange(1, kv + 1)[None, :]) < 0] = 0.0
-        bwd[:, 1 : kv + 1] = U
-    return fwd, bwd, fs, bs
+        bwd[:, 0:kv] = U
+    return fwd, bwd, fs, bs, klp, kvp
 
 
 def lu_b0(B0, precomputed=None):

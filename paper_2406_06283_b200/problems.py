@@ -66,6 +66,11 @@ CONFIGS = {
                           coeff_lo=1.0, coeff_hi=10.0, coeff_seed=5, rhs="normal", rhs_seed=5000, nrhs=16),
     "5-32": ProblemConfig("5-32", n=1024, k=100.0, M=32, layers=4, cap=15, coeff="loguniform", coeff_cells=64,
                           coeff_lo=1.0, coeff_hi=10.0, coeff_seed=5, rhs="normal", rhs_seed=5000, nrhs=16),
+    # not a BASELINE config: a quarter-size stand-in with config 5-16's per-subdomain shape
+    # (64-cell boxes, overlap 4 -> ~5000-dof blocks, kl = 72), for profiler runs
+    "prof-512": ProblemConfig("prof-512", n=512, k=100.0, M=8, layers=4, cap=60, coeff="loguniform",
+                              coeff_cells=32, coeff_lo=1.0, coeff_hi=10.0, coeff_seed=5, rhs="normal",
+                              rhs_seed=5000, cstab=4.0),
 }
 
 

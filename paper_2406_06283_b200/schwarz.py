@@ -238,10 +238,10 @@ class TwoLevelPreconditioner:
         fwd_parts, bwd_parts, foff, boff = [], [], [], []
         fpos = bpos = 0
         for idof, f in factors:
-            fw, bw, fs, bs = pack_band_records(f)
+            fw, bw, fs, bs, klp, kvp = pack_band_records(f)
             ns.append(f.n)
-            kls.append(f.kl)
-            kvs.append(f.kv)
+            kls.append(klp)
+            kvs.append(kvp)
             fss.append(fs)
             bss.append(bs)
             idx_off.append(idx_off[-1] + idof.size)

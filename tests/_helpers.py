@@ -19,17 +19,17 @@ def emulate_band_records(fwd, bwd, n, kl, kv, r):
     b = np.array(r, dtype=float, copy=True)
     for j in range(n):
         rec = fwd[j]
-        l = int(round(rec[0]))
+        l = int(round(rec[kl]))
         if l != j:
             b[j], b[l] = b[l], b[j]
         t1 = min(kl, n - 1 - j)
         if t1 > 0:
-            b[j + 1 : j + 1 + t1] -= rec[1 : 1 + t1] * b[j]
+            b[j + 1 : j + 1 + t1] -= rec[0:t1] * b[j]
     for rr in range(n):
         j = n - 1 - rr
         rec = bwd[rr]
-        b[j] = b[j] * rec[0]
+        b[j] = b[j] * rec[kv]
         t1 = min(kv, j)
         if t1 > 0:
-            b[j - t1 : j][::-1] -= rec[1 : 1 + t1] * b[j]
+            b[j - t1 : j][::-1] -= rec[0:t1] * b[j]
     return b

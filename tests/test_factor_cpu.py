@@ -20,7 +20,7 @@ def _banded(rng, n, w, weak_diag=False):
     return sp.csr_matrix(A)
 
 
-@pytest.mark.parametrize("n,w,weak", [(7, 2, False), (50, 5, True), (97, 24, True), (130, 40, False)])
+@pytest.mark.parametrize("n,w,weak", [(5, 1, False), (7, 2, False), (50, 5, True), (97, 24, True), (130, 40, False)])
 def test_records_match_dgbtrs(n, w, weak):
     rng = np.random.default_rng(n)
     A = _banded(rng, n, w, weak)
@@ -28,10 +28,11 @@ def test_records_match_dgbtrs(n, w, weak):
     assert f.kl == w and f.ku == w
     if weak:
         assert np.any(f.piv != np.arange(n))
-    fwd, bwd, fs, bs = factor.pack_band_records(f)
-    assert fs % 2 == 0 and bs % 2 == 0 and fs >= f.kl + 1 and bs >= f.kv + 1
+    fwd, bwd, fs, bs, klp, kvp = factor.pack_band_records(f)
+    assert fs % 2 == 0 and bs % 2 == 0 and fs >= klp + 1 and bs >= kvp + 1
+    assert klp >= max(f.kl, 3) and kvp >= max(f.kv, 3)
     b = rng.standard_normal(n)
-    x_rec = emulate_band_records(fwd, bwd, n, f.kl, f.kv, b)
+    x_rec = emulate_band_records(fwd, bwd, n, klp, kvp, b)
     x_lap = f.solve(b)
     x_dense = np.linalg.solve(A.toarray(), b)
     assert np.abs(x_rec - x_lap).max() <= 1e-12 * np.abs(x_lap).max()
@@ -46,9 +47,9 @@ def test_helmholtz_blocks_match_superlu(golden):
     for i, j, sub in list(P.dec.fine_flat())[:4]:
         blk = B[sub.idof][:, sub.idof]
         f = factor.band_lu(blk, label=(i, j))
-        fwd, bwd, _, _ = factor.pack_band_records(f)
+        fwd, bwd, _, _, klp, kvp = factor.pack_band_records(f)
         r = np.random.default_rng(i).standard_normal(sub.idof.size)
-        x = emulate_band_records(fwd, bwd, f.n, f.kl, f.kv, r)
+        x = emulate_band_records(fwd, bwd, f.n, klp, kvp, r)
         ref = spla.splu(blk.tocsc()).solve(r)
         assert np.abs(x - ref).max() <= 1e-11 * np.abs(ref).max()
 

@@ -11,7 +11,7 @@ import paper_2406_06283_b200 as hg
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "5-16"
 n_apply = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-P = hg.build_problem(cfg, cstab="cache")
+P = hg.build_problem(cfg, cstab=None if cfg.startswith("prof") else "cache", workers=int(os.environ.get("SETUP_WORKERS", "0")) or None)
 pre = hg.factorize(P.forms, P.dec, P.coarse)
 r = torch.from_numpy(np.random.default_rng(0).standard_normal(pre.n)).cuda()
 for _ in range(n_apply):
