@@ -247,10 +247,11 @@ def build_problem(cfg, gevp="auto", workers=None, one_level=False, verbose=False
     t0 = time.perf_counter()
     dec = _decomp.build_two_level(mesh, space, cfg.M, cfg.q, cfg.layers, cfg.layers)
     tick("decomp", t0)
+    cstab_arg = cstab
     results, selection, coarse, cstab, tau_target = [], None, None, float("nan"), float("nan")
     if not one_level:
         t0 = time.perf_counter()
-        mode = cfg.cstab if cstab is None else cstab
+        mode = cfg.cstab if cstab_arg is None else cstab_arg
         if mode == "cache":
             val = cached_cstab(cfg)
             cstab = float(val) if val is not None else estimate_cstab_sparse(forms)
