@@ -96,10 +96,13 @@ typedef struct {
    * dense row-major blocks Z_b (cblk_n[b] x cblk_m[b]) over the index sets
    * cblk_idx[cblk_idx_off[b] ..]; columns are numbered block after block
    * (the reference's column order, eigencoarse.py:259-266).
-   * B0 = P^T L U (LAPACK getrf); (P c)[i] = c[b0_perm[i]].  L (unit lower,
-   * bandwidth b0_kl) and U (bandwidth b0_ku) are stored row-major in band
-   * form: lband[i*b0_kl + t] = L[i][i-b0_kl+t] (t < b0_kl),
-   *       uband[i*(b0_ku+1) + t] = U[i][i+t]     (t <= b0_ku). */
+   * B0 = P^T L U (LAPACK getrf); (P c)[i] = c[b0_perm[i]].  The two
+   * triangular solves (L; then U in reversed coordinates, where it is lower
+   * triangular) are cut into b0_npanel panels of b0_panel rows each (m padded
+   * with identity rows).  Panel g = phase*K + t has the explicit inverse of
+   * its diagonal block at b0_dinv[g*P*P] (row-major) and the nonzero
+   * off-diagonal tiles b0_tiles[e*P*P] for e in [b0_tile_ptr[g],
+   * b0_tile_ptr[g+1]), column panel b0_tile_col[e] ascending. */
   int32_t m;
   int32_t n_cblk;
   const int32_t* cblk_n;
@@ -110,10 +113,14 @@ typedef struct {
   int64_t z_len;
   const double* z_data;
   const int32_t* b0_perm;
-  int32_t b0_kl;
-  int32_t b0_ku;
-  const double* b0_lband;
-  const double* b0_uband;
+  int32_t b0_panel;     /* P: 32, 64 or 128 */
+  int32_t b0_npanel;    /* K = ceil(m / P) */
+  const double* b0_dinv;        /* 2*K*P*P */
+  const int64_t* b0_tile_ptr;   /* 2*K+1 */
+  const int32_t* b0_tile_col;   /* ntile */
+  int64_t b0_ntile;
+  const double* b0_tiles;       /* ntile*P*P */
+  int32_t b0_ctas;      /* persistent CTAs of the coarse solve (0 = default 32) */
 } HgPrecondDesc;
 
 /* ---- library ---- */

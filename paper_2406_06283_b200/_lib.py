@@ -50,10 +50,14 @@ class HgPrecondDesc(ctypes.Structure):
         ("z_len", ctypes.c_int64),
         ("z_data", _f64p),
         ("b0_perm", _i32p),
-        ("b0_kl", ctypes.c_int32),
-        ("b0_ku", ctypes.c_int32),
-        ("b0_lband", _f64p),
-        ("b0_uband", _f64p),
+        ("b0_panel", ctypes.c_int32),
+        ("b0_npanel", ctypes.c_int32),
+        ("b0_dinv", _f64p),
+        ("b0_tile_ptr", _i64p),
+        ("b0_tile_col", _i32p),
+        ("b0_ntile", ctypes.c_int64),
+        ("b0_tiles", _f64p),
+        ("b0_ctas", ctypes.c_int32),
     ]
 
 

@@ -195,8 +195,12 @@ int hg_precond_destroy(HgPrecond* P) {
   release(P->d_col_blk);
   release(P->d_zt_items);
   release(P->d_b0_perm);
-  release(P->d_lband);
-  release(P->d_uband);
+  release(P->d_b0_dinv);
+  release(P->d_b0_tile_ptr);
+  release(P->d_b0_tile_col);
+  release(P->d_b0_tiles);
+  release(P->d_b0_x);
+  release(P->d_b0_done);
   release(P->d_y);
   release(P->d_zs);
   release(P->d_cptr);
@@ -337,10 +341,25 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
     HG_TRY(upload(&P->d_col_blk, col_blk.data(), col_blk.size(), bytes));
     HG_TRY(upload(&P->d_zt_items, items.data(), items.size(), bytes));
     HG_TRY(upload(&P->d_b0_perm, D->b0_perm, (size_t)P->m, bytes));
-    P->b0_kl = D->b0_kl;
-    P->b0_ku = D->b0_ku;
-    HG_TRY(upload(&P->d_lband, D->b0_lband, (size_t)P->m * D->b0_kl, bytes));
-    HG_TRY(upload(&P->d_uband, D->b0_uband, (size_t)P->m * (D->b0_ku + 1), bytes));
+    const int bp = D->b0_panel, bk = D->b0_npanel;
+    if ((bp != 32 && bp != 64 && bp != 128) || (long long)bk * bp < P->m || (long long)(bk - 1) * bp >= P->m ||
+        !D->b0_dinv || !D->b0_tile_ptr || D->b0_tile_ptr[2 * bk] != D->b0_ntile) {
+      set_error("hg_precond_create: inconsistent coarse tile description");
+      return HG_ERR_ARG;
+    }
+    P->b0_P = bp;
+    P->b0_K = bk;
+    P->b0_ctas = D->b0_ctas > 0 ? D->b0_ctas : 32;
+    HG_TRY(upload(&P->d_b0_dinv, D->b0_dinv, (size_t)2 * bk * bp * bp, bytes));
+    HG_TRY(upload(&P->d_b0_tile_ptr, reinterpret_cast<const long long*>(D->b0_tile_ptr), (size_t)2 * bk + 1, bytes));
+    if (D->b0_ntile > 0) {
+      HG_TRY(upload(&P->d_b0_tile_col, D->b0_tile_col, (size_t)D->b0_ntile, bytes));
+      HG_TRY(upload(&P->d_b0_tiles, D->b0_tiles, (size_t)D->b0_ntile * bp * bp, bytes));
+    }
+    HG_TRY(upload<double>(&P->d_b0_x, nullptr, (size_t)2 * bk * bp, bytes));
+    HG_TRY(upload<unsigned long long>(&P->d_b0_done, nullptr, 1, bytes));
+    HG_CUDA_TRY(cudaMemset(P->d_b0_done, 0, sizeof(unsigned long long)));
+    P->b0_epoch = 0;
     HG_TRY(upload<double>(&P->d_y, nullptr, (size_t)P->m, bytes));
     HG_TRY(upload<double>(&P->d_zs, nullptr, (size_t)std::max(nidx, 1LL), bytes));
     std::vector<int> ptr;

@@ -4,13 +4,7 @@
 //         dense row-major per-subdomain blocks on the coarse idof; each CTA
 //         reduces a 256-row chunk of one block to a partial vector.
 //  K_b0   y = B0^{-1} c      (schwarz.py:56, `lu_solve(self.b0_piv, .)`):
-//         sum the chunk partials, apply the getrf row permutation as a
-//         gather, then unit-lower and upper band triangular solves with the
-//         LU factors.  Dense LAPACK factors of the block-sparse B0 are
-//         banded (exact zeros outside the band), so only the band is stored
-//         and read.  Left-looking 32-row panels: a warp-per-row GEMV against
-//         the already solved part, then an in-register solve of the 32x32
-//         diagonal block.
+//         hg_b0.cu (tiled getrf factors, persistent multi-CTA solve).
 //  K_zy   u_b = Z_b y_b      (schwarz.py:57, `self.Z @ y`), one warp per row.
 //  K_asm  out[d] = sum_b u_b[d] + sum_s x_s[d]: coarse part first, then the
 //         local solutions in subdomain order — the reference's fixed
@@ -50,102 +44,6 @@ __global__ void __launch_bounds__(256) k_zt(const int2* __restrict__ items, cons
 int launch_zt(HgPrecond* P, const double* r, cudaStream_t st) {
   if (P->m == 0 || P->n_zt_items == 0) return HG_OK;
   k_zt<<<P->n_zt_items, 256, 0, st>>>(P->d_zt_items, P->d_cblk, P->d_cblk_idx, P->d_z, r, P->d_cpart);
-  HG_LAUNCH_CHECK();
-  return HG_OK;
-}
-
-constexpr int B0_THREADS = 1024;
-constexpr int B0_PANEL = 32;
-
-__global__ void __launch_bounds__(B0_THREADS) k_b0_solve(int m, const int* __restrict__ perm,
-                                                         const int* __restrict__ col_blk,
-                                                         const CblkDesc* __restrict__ descs,
-                                                         const double* __restrict__ cpart, int kl,
-                                                         const double* __restrict__ lband, int ku,
-                                                         const double* __restrict__ uband,
-                                                         double* __restrict__ y) {
-  extern __shared__ double x[];  // m
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // c = Z^T r (sum of chunk partials in chunk order), then x = P c
-  for (int i = tid; i < m; i += B0_THREADS) {
-    const int col = perm[i];
-    const CblkDesc d = descs[col_blk[col]];
-    const int l = col - d.col0;
-    double c = 0.0;
-    for (int ch = 0; ch < d.nchunk; ++ch) c += cpart[d.part_off + (long long)ch * d.m + l];
-    x[i] = c;
-  }
-  __syncthreads();
-  // ---- L solve (unit lower, bandwidth kl), panels top to bottom
-  for (int p0 = 0; p0 < m; p0 += B0_PANEL) {
-    const int i = p0 + warp;  // one row per warp
-    if (i < m && p0 > 0) {
-      const int jlo = max(0, i - kl);
-      const double* li = lband + (long long)i * kl - (i - kl);  // li[j] = L[i][j]
-      double acc = 0.0;
-      for (int j = jlo + lane; j < p0; j += 32) acc = fma(li[j], x[j], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) x[i] -= acc;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      const int row = p0 + lane;
-      double v = row < m ? x[row] : 0.0;
-      const double* lr = lband + (long long)row * kl - (row - kl);
-#pragma unroll 4
-      for (int jj = 0; jj < B0_PANEL - 1; ++jj) {
-        const double xj = __shfl_sync(FULL, v, jj);
-        if (lane > jj && row < m && lane - jj <= kl) v = fma(-lr[p0 + jj], xj, v);
-      }
-      if (row < m) x[row] = v;
-    }
-    __syncthreads();
-  }
-  // ---- U solve (upper, bandwidth ku incl. pivot fill), panels bottom to top
-  const int np = (m + B0_PANEL - 1) / B0_PANEL;
-  for (int pb = np - 1; pb >= 0; --pb) {
-    const int p0 = pb * B0_PANEL, p1 = min(m, p0 + B0_PANEL);
-    const int i = p0 + warp;
-    if (i < p1 && p1 < m) {
-      const int jhi = min(m - 1, i + ku);
-      const double* ui = uband + (long long)i * (ku + 1) - i;  // ui[j] = U[i][j]
-      double acc = 0.0;
-      for (int j = p1 + lane; j <= jhi; j += 32) acc = fma(ui[j], x[j], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) x[i] -= acc;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      const int row = p0 + lane;
-      double v = row < m ? x[row] : 0.0;
-      const double* ur = uband + (long long)row * (ku + 1) - row;
-      for (int jj = B0_PANEL - 1; jj >= 0; --jj) {
-        if (p0 + jj >= m) continue;  // uniform
-        if (lane == jj) v = v / ur[row];
-        const double xj = __shfl_sync(FULL, v, jj);
-        if (lane < jj && jj - lane <= ku) v = fma(-ur[p0 + jj], xj, v);
-      }
-      if (row < m) x[row] = v;
-    }
-    __syncthreads();
-  }
-  for (int i = tid; i < m; i += B0_THREADS) y[i] = x[i];
-}
-
-int launch_coarse_solve(HgPrecond* P, cudaStream_t st) {
-  if (P->m == 0) return HG_OK;
-  const size_t smem = sizeof(double) * (size_t)P->m;
-  if (smem > 227 * 1024) {
-    set_error("coarse solve: m too large for the single-CTA band solver");
-    return HG_ERR_UNSUPPORTED;
-  }
-  static size_t configured = 0;
-  if (configured < smem) {
-    HG_CUDA_TRY(cudaFuncSetAttribute(k_b0_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
-  k_b0_solve<<<1, B0_THREADS, smem, st>>>(P->m, P->d_b0_perm, P->d_col_blk, P->d_cblk, P->d_cpart,
-                                           P->b0_kl, P->d_lband, P->b0_ku, P->d_uband, P->d_y);
   HG_LAUNCH_CHECK();
   return HG_OK;
 }

@@ -64,9 +64,14 @@ struct HgPrecond {
   int2* d_zt_items = nullptr;     // (block, row chunk) work items of Z^T r and Z y
   int n_zt_items = 0;
   int* d_b0_perm = nullptr;
-  int b0_kl = 0, b0_ku = 0;
-  double* d_lband = nullptr;
-  double* d_uband = nullptr;
+  int b0_P = 0, b0_K = 0, b0_ctas = 32;   // panel size, panels per phase, persistent CTAs
+  unsigned long long b0_epoch = 0;        // value of the completion counter at the next launch
+  double* d_b0_dinv = nullptr;            // [2][K][P][P]
+  long long* d_b0_tile_ptr = nullptr;     // [2K+1]
+  int* d_b0_tile_col = nullptr;
+  double* d_b0_tiles = nullptr;           // [ntile][P][P]
+  double* d_b0_x = nullptr;               // [2][K*P] phase solutions
+  unsigned long long* d_b0_done = nullptr;  // monotone panel completion counter
   double* d_y = nullptr;          // coarse solution (m)
   long long zs_len = 0;
   double* d_zs = nullptr;         // per-block Z_b y_b rows (scratch)

@@ -168,6 +168,111 @@ def perm_from_piv(piv):
     return p
 
 
+@dataclass
+class B0Tiles:
+    """Panel-tiled getrf factors of B0 for the device coarse solve.
+
+    Phase 0 solves L x = P c (unit lower), phase 1 solves U y = x in reversed
+    coordinates (J U J is lower triangular), both padded to K = ceil(m/P)
+    panels of P rows (padding: identity rows, zero right-hand side).  Per
+    phase and panel t: ``dinv[phase, t]`` = inverse of the P x P diagonal
+    block, and the nonzero off-diagonal tiles T[t, j] (j < t, ascending) in
+    ``tiles[tile_ptr[phase*K + t] : tile_ptr[phase*K + t + 1]]`` with their
+    column panel in ``tile_col``.  Tiles that are entirely zero are skipped.
+    """
+
+    m: int
+    P: int
+    K: int
+    perm: np.ndarray
+    dinv: np.ndarray      # (2, K, P, P)
+    tile_ptr: np.ndarray  # (2K + 1,) int64
+    tile_col: np.ndarray  # (ntile,) int32
+    tiles: np.ndarray     # (ntile, P, P)
+
+    @property
+    def nbytes(self):
+        return self.dinv.nbytes + self.tiles.nbytes
+
+    def solve(self, c):
+        """Host emulation of the device algorithm (for parity checks)."""
+        K, P, m = self.K, self.P, self.m
+        mp = K * P
+        rhs = np.zeros(mp)
+        rhs[:m] = np.asarray(c)[self.perm]
+        x = [np.zeros(mp), np.zeros(mp)]
+        for ph in range(2):
+            if ph == 1:
+                rhs = x[0][::-1].copy()
+            for t in range(K):
+                acc = rhs[t * P:(t + 1) * P].copy()
+                for e in range(self.tile_ptr[ph * K + t], self.tile_ptr[ph * K + t + 1]):
+                    j = self.tile_col[e]
+                    acc -= self.tiles[e] @ x[ph][j * P:(j + 1) * P]
+                x[ph][t * P:(t + 1) * P] = self.dinv[ph, t] @ acc
+        return x[1][::-1][:m].copy()
+
+
+def pack_b0_tiles(lu, piv, P=64):
+    """B0Tiles from dense getrf factors (lu, piv)."""
+    m = lu.shape[0]
+    K = (m + P - 1) // P
+    mp = K * P
+    perm = perm_from_piv(np.asarray(piv))
+    dinv = np.zeros((2, K, P, P))
+    ptr = [0]
+    cols, tiles = [], []
+    for ph in range(2):
+        for t in range(K):
+            r0, r1 = t * P, min(m, (t + 1) * P)
+            if ph == 0:
+                rows = np.arange(r0, r1)
+            else:
+                # reversed coordinates: row a of J U J is row mp-1-a of U (padding first)
+                rows = mp - 1 - np.arange(t * P, (t + 1) * P)
+            D = np.eye(P)
+            for j in range(t + 1):
+                c0 = j * P
+                if ph == 0:
+                    cidx = np.arange(c0, c0 + P)
+                    valid_c = cidx < m
+                    blk = np.zeros((P, P))
+                    rr = rows
+                    sub = lu[np.ix_(rr, cidx[valid_c])]
+                    if j == t:
+                        sub = np.tril(sub, -1) + np.eye(sub.shape[0], sub.shape[1])
+                    else:
+                        pass
+                    blk[: rr.size, : valid_c.sum()] = sub
+                else:
+                    cidx = mp - 1 - np.arange(c0, c0 + P)
+                    vr = rows < m
+                    vc = cidx < m
+                    blk = np.zeros((P, P))
+                    if vr.any() and vc.any():
+                        sub = lu[np.ix_(rows[vr], cidx[vc])]
+                        blk[np.ix_(np.flatnonzero(vr), np.flatnonzero(vc))] = sub
+                    if j == t:
+                        blk = np.tril(blk)  # J U J is lower triangular
+                if j == t:
+                    if ph == 0:
+                        D[: blk.shape[0], : blk.shape[1]] = 0.0
+                        D = np.eye(P)
+                        D[: rows.size, : rows.size] = blk[: rows.size, : rows.size]
+                    else:
+                        pad = ~(rows < m)
+                        blk[np.flatnonzero(pad), np.flatnonzero(pad)] = 1.0
+                        D = blk
+                    dinv[ph, t] = scipy.linalg.solve_triangular(D, np.eye(P), lower=True,
+                                                                unit_diagonal=(ph == 0))
+                elif np.any(blk):
+                    cols.append(j)
+                    tiles.append(blk)
+            ptr.append(len(cols))
+    tiles = np.ascontiguousarray(np.array(tiles).reshape(len(tiles), P, P)) if tiles else np.zeros((0, P, P))
+    return B0Tiles(m, P, K, perm, dinv, np.asarray(ptr, dtype=np.int64), np.asarray(cols, dtype=np.int32), tiles)
+
+
 def pack_b0(lu, piv, row_block=1024):
     """Band widths and row-major band storage of the getrf factors.
 

@@ -15,6 +15,7 @@ no CPU path: without the library or a GPU the calls raise.
 """
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -23,7 +24,7 @@ import scipy.sparse as sp
 
 from . import _lib
 from .errors import SingularOperatorError
-from .factor import band_lu, lu_b0, pack_b0, pack_band_records, submatrix
+from .factor import band_lu, lu_b0, pack_b0_tiles, pack_band_records, submatrix
 
 _DENSE_EIG_LIMIT = 1500
 
@@ -275,9 +276,19 @@ class TwoLevelPreconditioner:
         self.cblock_shapes = [b.shape for _, b in cblocks]
         self.b0_bytes = 0
         if m:
-            perm, kl, ku, lband, uband = pack_b0(lu, piv)
-            self.b0_band = (kl, ku)
-            self.b0_bytes = 8 * m * (kl + ku + 1) + 4 * m
+            P = int(os.environ.get("HG_B0_PANEL", "64"))
+            T = pack_b0_tiles(lu, piv, P)
+            # guard: the tiled algorithm (inverted diagonal blocks) must agree with getrs
+            c = np.random.default_rng(0).standard_normal(m)
+            want = scipy.linalg.lu_solve((lu, piv), c)
+            dev = float(np.abs(T.solve(c) - want).max() / max(np.abs(want).max(), 1e-300))
+            if dev > 1e-11:
+                raise SingularOperatorError(
+                    "coarse tile factorisation deviates from getrs by %.2e (B0 too ill-conditioned for "
+                    "inverted %dx%d diagonal blocks)" % (dev, P, P))
+            self.b0_tiles = T
+            self.b0_tile_dev = dev
+            self.b0_bytes = T.nbytes + 4 * m + 4 * T.tile_col.size
             d.n_cblk = len(cblocks)
             d.cblk_n = arr([i.size for i, _ in cblocks], np.int32, i32)
             d.cblk_m = arr([b.shape[1] for _, b in cblocks], np.int32, i32)
@@ -288,11 +299,15 @@ class TwoLevelPreconditioner:
             z = np.concatenate([b.ravel() for _, b in cblocks])
             d.z_len = z.size
             d.z_data = arr(z, np.float64, f64)
-            d.b0_perm = arr(perm, np.int32, i32)
-            d.b0_kl = kl
-            d.b0_ku = ku
-            d.b0_lband = arr(lband if kl else np.zeros(1), np.float64, f64)
-            d.b0_uband = arr(uband, np.float64, f64)
+            d.b0_perm = arr(T.perm, np.int32, i32)
+            d.b0_panel = T.P
+            d.b0_npanel = T.K
+            d.b0_dinv = arr(T.dinv, np.float64, f64)
+            d.b0_tile_ptr = arr(T.tile_ptr, np.int64, i64)
+            d.b0_tile_col = arr(T.tile_col if T.tile_col.size else np.zeros(1), np.int32, i32)
+            d.b0_ntile = int(T.tile_col.size)
+            d.b0_tiles = arr(T.tiles if T.tiles.size else np.zeros(1), np.float64, f64)
+            d.b0_ctas = int(os.environ.get("HG_B0_CTAS", "0"))
         h = ctypes.c_void_p()
         _lib.check(lib.hg_precond_create(ctypes.byref(d), ctypes.byref(h)), "hg_precond_create")
         self._handle = h
