@@ -121,6 +121,15 @@ typedef struct {
   int64_t b0_ntile;
   const double* b0_tiles;       /* ntile*P*P */
   int32_t b0_ctas;      /* persistent CTAs of the coarse solve (0 = default 32) */
+  /* b0_mode 0: persistent-CTA solve synchronised through an L2 counter;
+   * b0_mode 1: single thread-block cluster of b0_cluster (<= 16) CTAs, panels
+   * handed over through distributed shared memory (ring of b0_ring panels;
+   * requires P = 64, b0_ring >= max tile distance + b0_cluster, and tiles /
+   * inverse blocks with 16-byte chunks XOR-swizzled by row parity:
+   * chunk c of row r stored at chunk c ^ ((r & 1) << 2)). */
+  int32_t b0_mode;
+  int32_t b0_cluster;
+  int32_t b0_ring;
 } HgPrecondDesc;
 
 /* ---- library ---- */

@@ -58,6 +58,9 @@ class HgPrecondDesc(ctypes.Structure):
         ("b0_ntile", ctypes.c_int64),
         ("b0_tiles", _f64p),
         ("b0_ctas", ctypes.c_int32),
+        ("b0_mode", ctypes.c_int32),
+        ("b0_cluster", ctypes.c_int32),
+        ("b0_ring", ctypes.c_int32),
     ]
 
 

@@ -78,12 +78,15 @@ struct HgOp {
 static int precond_apply_core(HgPrecond* P, const double* r, double* out, const double* W, long long ldw,
                               int nv, double* partials, int* nb, cudaStream_t st) {
   if (P->m > 0) {
+    // The latency-bound coarse solve is launched FIRST (side stream) so that
+    // it holds its SMs before the local solves fill the GPU; it starts its
+    // work when this apply's Z^T r chunks are all counted (device-side wait).
     HG_CUDA_TRY(cudaEventRecord(P->ev_fork, st));
     HG_CUDA_TRY(cudaStreamWaitEvent(P->aux, P->ev_fork, 0));
-    HG_TRY(launch_zt(P, r, P->aux));
-    HG_TRY(launch_coarse_solve(P, P->aux));
+    HG_TRY(launch_coarse_solve(P, P->aux, P->zt_epoch + (unsigned long long)P->n_zt_items));
     HG_TRY(launch_zy(P, P->aux));
     HG_CUDA_TRY(cudaEventRecord(P->ev_join, P->aux));
+    HG_TRY(launch_zt(P, r, st));
   }
   HG_TRY(launch_local_solve(P, r, st));
   if (P->m > 0) HG_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_join, 0));
@@ -201,6 +204,7 @@ int hg_precond_destroy(HgPrecond* P) {
   release(P->d_b0_tiles);
   release(P->d_b0_x);
   release(P->d_b0_done);
+  release(P->d_zt_done);
   release(P->d_y);
   release(P->d_zs);
   release(P->d_cptr);
@@ -350,6 +354,16 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
     P->b0_P = bp;
     P->b0_K = bk;
     P->b0_ctas = D->b0_ctas > 0 ? D->b0_ctas : 32;
+    P->b0_mode = D->b0_mode;
+    if (P->b0_mode == 1) {
+      P->b0_cs = D->b0_cluster;
+      P->b0_nr = D->b0_ring;
+      if (bp != 64 || P->b0_cs < 1 || P->b0_cs > 16 || P->b0_nr < P->b0_cs + 1 ||
+          b0_cluster_smem(P->b0_nr) > 227 * 1024) {
+        set_error("hg_precond_create: invalid cluster coarse-solve parameters");
+        return HG_ERR_ARG;
+      }
+    }
     HG_TRY(upload(&P->d_b0_dinv, D->b0_dinv, (size_t)2 * bk * bp * bp, bytes));
     HG_TRY(upload(&P->d_b0_tile_ptr, reinterpret_cast<const long long*>(D->b0_tile_ptr), (size_t)2 * bk + 1, bytes));
     if (D->b0_ntile > 0) {
@@ -359,6 +373,9 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
     HG_TRY(upload<double>(&P->d_b0_x, nullptr, (size_t)2 * bk * bp, bytes));
     HG_TRY(upload<unsigned long long>(&P->d_b0_done, nullptr, 1, bytes));
     HG_CUDA_TRY(cudaMemset(P->d_b0_done, 0, sizeof(unsigned long long)));
+    HG_TRY(upload<unsigned long long>(&P->d_zt_done, nullptr, 1, bytes));
+    HG_CUDA_TRY(cudaMemset(P->d_zt_done, 0, sizeof(unsigned long long)));
+    P->zt_epoch = 0;
     P->b0_epoch = 0;
     HG_TRY(upload<double>(&P->d_y, nullptr, (size_t)P->m, bytes));
     HG_TRY(upload<double>(&P->d_zs, nullptr, (size_t)std::max(nidx, 1LL), bytes));
@@ -368,6 +385,11 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
     HG_TRY(upload(&P->d_cptr, ptr.data(), ptr.size(), bytes));
     HG_TRY(upload(&P->d_cent, ent.data(), ent.size(), bytes));
   }
+  HG_TRY(preload_local(P));
+  HG_TRY(preload_coarse());
+  HG_TRY(preload_assemble());
+  HG_TRY(preload_b0());
+  HG_TRY(preload_vec());
   HG_CUDA_TRY(cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking));
   HG_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
   HG_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
@@ -419,7 +441,7 @@ int hg_precond_apply_coarse(HgPrecond* P, const double* r, double* out, void* st
   cudaStream_t st = (cudaStream_t)stream;
   if (P->m == 0) return launch_fill(P->n, out, 0.0, st);
   HG_TRY(launch_zt(P, r, st));
-  HG_TRY(launch_coarse_solve(P, st));
+  HG_TRY(launch_coarse_solve(P, st, P->zt_epoch));
   HG_TRY(launch_zy(P, st));
   return launch_assemble(P, true, false, out, nullptr, 0, 0, nullptr, nullptr, st);
 }
@@ -439,7 +461,7 @@ int hg_precond_profile(HgPrecond* P, const double* r, double* out, int32_t iters
     cudaEventRecord(ev[0], st);
     if ((status = launch_zt(P, r, st)) != HG_OK) break;
     cudaEventRecord(ev[1], st);
-    if ((status = launch_coarse_solve(P, st)) != HG_OK) break;
+    if ((status = launch_coarse_solve(P, st, P->zt_epoch)) != HG_OK) break;
     cudaEventRecord(ev[2], st);
     if ((status = launch_zy(P, st)) != HG_OK) break;
     cudaEventRecord(ev[3], st);

@@ -56,7 +56,9 @@ __global__ void __launch_bounds__(THREADS) k_b0_tiles(int m, int K, const int* _
                                                       const int* __restrict__ tile_col,
                                                       const double* __restrict__ tiles, double* xbuf,
                                                       unsigned long long* done, unsigned long long base,
-                                                      double* __restrict__ y) {
+                                                      double* __restrict__ y,
+                                                      const unsigned long long* zt_done,
+                                                      unsigned long long zt_target) {
   constexpr int TPR = THREADS / P;  // threads per row
   constexpr int CPT = P / TPR;      // columns per thread
   static_assert(TPR >= 1 && TPR <= 32 && (32 % TPR) == 0 && CPT % 2 == 0, "tile mapping");
@@ -75,6 +77,10 @@ __global__ void __launch_bounds__(THREADS) k_b0_tiles(int m, int K, const int* _
     __syncthreads();
     return s_seen;
   };
+  if (tid == 0)  // c = Z^T r of this apply complete (the solve may be launched before it)
+    while (ld_acquire_u64(zt_done) < zt_target) {
+    }
+  __syncthreads();
   for (int g = blockIdx.x; g < 2 * K; g += gridDim.x) {
     const int ph = g / K, t = g % K;
     const bool stamp = g_b0_stamp_on && tid == 0 && g < B0_MAX_STAMPED;
@@ -168,8 +174,17 @@ __global__ void __launch_bounds__(THREADS) k_b0_tiles(int m, int K, const int* _
   }
 }
 
-int launch_coarse_solve(HgPrecond* P, cudaStream_t st) {
+int preload_b0() {
+  cudaFuncAttributes at;
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_b0_tiles<64, 256>));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_b0_tiles<128, 512>));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_b0_tiles<32, 128>));
+  return preload_b0_cluster();
+}
+
+int launch_coarse_solve(HgPrecond* P, cudaStream_t st, unsigned long long zt_target) {
   if (P->m == 0) return HG_OK;
+  if (P->b0_mode == 1) return launch_coarse_solve_cluster(P, st, zt_target);
   const int K = P->b0_K;
   const int G = K < P->b0_ctas ? K : P->b0_ctas;
   const unsigned long long base = P->b0_epoch;
@@ -178,17 +193,17 @@ int launch_coarse_solve(HgPrecond* P, cudaStream_t st) {
     case 64:
       k_b0_tiles<64, 256><<<G, 256, 0, st>>>(P->m, K, P->d_b0_perm, P->d_col_blk, P->d_cblk, P->d_cpart,
                                               P->d_b0_dinv, P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles,
-                                              P->d_b0_x, P->d_b0_done, base, P->d_y);
+                                              P->d_b0_x, P->d_b0_done, base, P->d_y, P->d_zt_done, zt_target);
       break;
     case 128:
       k_b0_tiles<128, 512><<<G, 512, 0, st>>>(P->m, K, P->d_b0_perm, P->d_col_blk, P->d_cblk, P->d_cpart,
                                                P->d_b0_dinv, P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles,
-                                               P->d_b0_x, P->d_b0_done, base, P->d_y);
+                                               P->d_b0_x, P->d_b0_done, base, P->d_y, P->d_zt_done, zt_target);
       break;
     case 32:
       k_b0_tiles<32, 128><<<G, 128, 0, st>>>(P->m, K, P->d_b0_perm, P->d_col_blk, P->d_cblk, P->d_cpart,
                                               P->d_b0_dinv, P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles,
-                                              P->d_b0_x, P->d_b0_done, base, P->d_y);
+                                              P->d_b0_x, P->d_b0_done, base, P->d_y, P->d_zt_done, zt_target);
       break;
     default:
       set_error("coarse solve: unsupported panel size");

@@ -19,7 +19,8 @@ constexpr int ZT_ROWS = 256;
 
 __global__ void __launch_bounds__(256) k_zt(const int2* __restrict__ items, const CblkDesc* __restrict__ descs,
                                             const int* __restrict__ idx, const double* __restrict__ Z,
-                                            const double* __restrict__ r, double* __restrict__ cpart) {
+                                            const double* __restrict__ r, double* __restrict__ cpart,
+                                            unsigned long long* __restrict__ done) {
   __shared__ double s[4][64];
   const int2 it = items[blockIdx.x];
   const CblkDesc d = descs[it.x];
@@ -39,12 +40,20 @@ __global__ void __launch_bounds__(256) k_zt(const int2* __restrict__ items, cons
       cpart[d.part_off + (long long)chunk * d.m + col] = ((s[0][cl] + s[1][cl]) + s[2][cl]) + s[3][cl];
     __syncthreads();
   }
+  // completion count: the coarse solve, launched earlier on another stream so
+  // that it holds its SMs, starts when every chunk of this apply is counted
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(done, 1ull);
+  }
 }
 
 int launch_zt(HgPrecond* P, const double* r, cudaStream_t st) {
   if (P->m == 0 || P->n_zt_items == 0) return HG_OK;
-  k_zt<<<P->n_zt_items, 256, 0, st>>>(P->d_zt_items, P->d_cblk, P->d_cblk_idx, P->d_z, r, P->d_cpart);
+  k_zt<<<P->n_zt_items, 256, 0, st>>>(P->d_zt_items, P->d_cblk, P->d_cblk_idx, P->d_z, r, P->d_cpart,
+                                        P->d_zt_done);
   HG_LAUNCH_CHECK();
+  P->zt_epoch += (unsigned long long)P->n_zt_items;
   return HG_OK;
 }
 
@@ -63,6 +72,13 @@ __global__ void __launch_bounds__(256) k_zy(const int2* __restrict__ items, cons
     acc = warp_sum(acc);
     if (lane == 0) zs[d.idx_off + k] = acc;
   }
+}
+
+int preload_coarse() {
+  cudaFuncAttributes at;
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_zt));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_zy));
+  return HG_OK;
 }
 
 int launch_zy(HgPrecond* P, cudaStream_t st) {
@@ -114,6 +130,12 @@ __global__ void __launch_bounds__(VEC_THREADS) k_assemble(int n, const int* __re
 }
 
 int assemble_nblocks(int n) { return ceil_div(n, VEC_TILE); }
+
+int preload_assemble() {
+  cudaFuncAttributes at;
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_assemble));
+  return HG_OK;
+}
 
 int launch_assemble(HgPrecond* P, bool with_coarse, bool with_local, double* out, const double* W,
                     long long ldw, int nv, double* partials, int* nblocks_out, cudaStream_t st) {

@@ -65,6 +65,8 @@ struct HgPrecond {
   int n_zt_items = 0;
   int* d_b0_perm = nullptr;
   int b0_P = 0, b0_K = 0, b0_ctas = 32;   // panel size, panels per phase, persistent CTAs
+  int b0_mode = 0;                        // 0: L2-counter kernel (hg_b0.cu), 1: cluster kernel (hg_b0c.cu)
+  int b0_cs = 0, b0_nr = 0;               // cluster size, x ring slots (mode 1)
   unsigned long long b0_epoch = 0;        // value of the completion counter at the next launch
   double* d_b0_dinv = nullptr;            // [2][K][P][P]
   long long* d_b0_tile_ptr = nullptr;     // [2K+1]
@@ -72,6 +74,9 @@ struct HgPrecond {
   double* d_b0_tiles = nullptr;           // [ntile][P][P]
   double* d_b0_x = nullptr;               // [2][K*P] phase solutions
   unsigned long long* d_b0_done = nullptr;  // monotone panel completion counter
+  unsigned long long* d_zt_done = nullptr;  // monotone count of finished Z^T r chunks
+  unsigned long long zt_epoch = 0;          // its value after the last launched Z^T r
+  unsigned long long b0_zt_target = 0;      // chunks the next coarse solve waits for
   double* d_y = nullptr;          // coarse solution (m)
   long long zs_len = 0;
   double* d_zs = nullptr;         // per-block Z_b y_b rows (scratch)
@@ -138,7 +143,17 @@ int spmv_dots_nblocks(int n);
 int launch_local_solve(HgPrecond* P, const double* r, cudaStream_t st);
 int launch_local_solve_single(HgPrecond* P, int s, const double* r_local, double* x_local, cudaStream_t st);
 int launch_zt(HgPrecond* P, const double* r, cudaStream_t st);
-int launch_coarse_solve(HgPrecond* P, cudaStream_t st);
+// zt_target: value of the Z^T r chunk counter the solve waits for before reading c
+int launch_coarse_solve(HgPrecond* P, cudaStream_t st, unsigned long long zt_target);
+int launch_coarse_solve_cluster(HgPrecond* P, cudaStream_t st, unsigned long long zt_target);
+size_t b0_cluster_smem(int NR);
+// force-load kernels at handle creation (see preload_local in hg_local.cu)
+int preload_local(HgPrecond* P);
+int preload_coarse();
+int preload_assemble();
+int preload_b0();
+int preload_b0_cluster();
+int preload_vec();
 int launch_zy(HgPrecond* P, cudaStream_t st);
 // out = coarse + local contributions; optional fused partial dots W[i].out
 int launch_assemble(HgPrecond* P, bool with_coarse, bool with_local, double* out, const double* W,

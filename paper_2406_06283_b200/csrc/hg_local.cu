@@ -311,6 +311,20 @@ static int launch_local_grid(HgPrecond* P, const LocalDesc* descs, int nblocks, 
   return HG_OK;
 }
 
+__global__ void k_scatter_local(int n, const int* __restrict__ idx, const double* __restrict__ src,
+                                double* __restrict__ dst);
+
+// CUDA lazy loading would load a kernel at its first launch, which waits for
+// running kernels — a deadlock when the spinning coarse solve is resident.
+// Every kernel the handle uses is loaded at creation instead.
+int preload_local(HgPrecond* P) {
+  cudaFuncAttributes at;
+  LocalKernel k = pick(P->rf, P->rb);
+  if (k) HG_CUDA_TRY(cudaFuncGetAttributes(&at, k));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_scatter_local));
+  return HG_OK;
+}
+
 int launch_local_solve(HgPrecond* P, const double* r, cudaStream_t st) {
   if (P->n_local == 0) return HG_OK;
   return launch_local_grid(P, P->d_local, P->n_local, r, st);

@@ -231,6 +231,20 @@ __global__ void k_fill(long long n, double* __restrict__ y, double v) {
   if (d < n) y[d] = v;
 }
 
+int preload_vec() {
+  cudaFuncAttributes at;
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_spmv));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_spmv_dots));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_dots));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_reduce_cols));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_axpy_multi));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_scale2));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_copy));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_sub));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_fill));
+  return HG_OK;
+}
+
 int launch_fill(long long n, double* y, double val, cudaStream_t st) {
   if (n == 0) return HG_OK;
   k_fill<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, y, val);

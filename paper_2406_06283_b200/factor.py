@@ -194,6 +194,8 @@ class B0Tiles:
     def nbytes(self):
         return self.dinv.nbytes + self.tiles.nbytes
 
+    premultiplied: bool = False  # tiles hold D_t^{-1} T[t, j] (cluster kernel form)
+
     def solve(self, c):
         """Host emulation of the device algorithm (for parity checks)."""
         K, P, m = self.K, self.P, self.m
@@ -205,12 +207,46 @@ class B0Tiles:
             if ph == 1:
                 rhs = x[0][::-1].copy()
             for t in range(K):
-                acc = rhs[t * P:(t + 1) * P].copy()
-                for e in range(self.tile_ptr[ph * K + t], self.tile_ptr[ph * K + t + 1]):
+                g = ph * K + t
+                if self.premultiplied:
+                    acc = self.dinv[ph, t] @ rhs[t * P:(t + 1) * P]
+                else:
+                    acc = rhs[t * P:(t + 1) * P].copy()
+                for e in range(self.tile_ptr[g], self.tile_ptr[g + 1]):
                     j = self.tile_col[e]
                     acc -= self.tiles[e] @ x[ph][j * P:(j + 1) * P]
-                x[ph][t * P:(t + 1) * P] = self.dinv[ph, t] @ acc
+                x[ph][t * P:(t + 1) * P] = acc if self.premultiplied else self.dinv[ph, t] @ acc
         return x[1][::-1][:m].copy()
+
+    def premultiply(self):
+        """Copy with every off-diagonal tile replaced by D_t^{-1} T[t, j]."""
+        tiles = self.tiles.copy()
+        for g in range(2 * self.K):
+            for e in range(self.tile_ptr[g], self.tile_ptr[g + 1]):
+                tiles[e] = self.dinv[g // self.K, g % self.K] @ self.tiles[e]
+        return B0Tiles(self.m, self.P, self.K, self.perm, self.dinv, self.tile_ptr, self.tile_col, tiles, True)
+
+
+def swizzle_tile_rows(arr):
+    """Row-parity XOR swizzle of 16-byte chunks used by the cluster coarse
+    kernel: chunk c of row r is stored at chunk c ^ ((r & 1) << 2)."""
+    arr = np.ascontiguousarray(arr)
+    P = arr.shape[-1]
+    a = arr.reshape(arr.shape[:-1] + (P // 2, 2))
+    out = a.copy()
+    perm = np.arange(P // 2) ^ 4
+    out[..., 1::2, :, :] = a[..., 1::2, perm, :]
+    return out.reshape(arr.shape)
+
+
+def tile_span(T):
+    """Largest distance t - j (in panels) between a panel and a tile it reads."""
+    span = 1
+    for g in range(2 * T.K):
+        e0, e1 = T.tile_ptr[g], T.tile_ptr[g + 1]
+        if e1 > e0:
+            span = max(span, int(g % T.K - T.tile_col[e0:e1].min()))
+    return span
 
 
 def pack_b0_tiles(lu, piv, P=64):

@@ -17,6 +17,7 @@ caps applied by truncation (D5), rtol 1e-6, x0 = 0, full GMRES.
 """
 
 import os
+import sys
 import time
 from concurrent.futures import ProcessPoolExecutor
 from dataclasses import dataclass, field
@@ -234,7 +235,7 @@ def build_problem(cfg, gevp="auto", workers=None, one_level=False, verbose=False
     def tick(name, t0):
         times[name] = time.perf_counter() - t0
         if verbose:
-            print("  setup %-9s %.2f s" % (name, times[name]), flush=True)
+            print("  setup %-9s %.2f s" % (name, times[name]), file=sys.stderr, flush=True)
 
     t0 = time.perf_counter()
     mesh = fem.build_unit_square_mesh(cfg.n)

@@ -24,7 +24,7 @@ import scipy.sparse as sp
 
 from . import _lib
 from .errors import SingularOperatorError
-from .factor import band_lu, lu_b0, pack_b0_tiles, pack_band_records, submatrix
+from .factor import band_lu, lu_b0, pack_b0_tiles, pack_band_records, submatrix, swizzle_tile_rows, tile_span
 
 _DENSE_EIG_LIMIT = 1500
 
@@ -278,6 +278,14 @@ class TwoLevelPreconditioner:
         if m:
             P = int(os.environ.get("HG_B0_PANEL", "64"))
             T = pack_b0_tiles(lu, piv, P)
+            # coarse-solve kernel: one DSMEM cluster when the x ring fits in shared memory
+            cs = min(16, T.K)
+            ring = tile_span(T) + cs + 1
+            mode = int(os.environ.get("HG_B0_MODE", "1"))
+            if mode == 1 and (T.P != 64 or ring > 96):  # the tagged x ring must fit in shared memory
+                mode = 0
+            if mode == 1:
+                T = T.premultiply()  # tiles D_t^{-1} T[t, j]: rows of a panel finish independently
             # guard: the tiled algorithm (inverted diagonal blocks) must agree with getrs
             c = np.random.default_rng(0).standard_normal(m)
             want = scipy.linalg.lu_solve((lu, piv), c)
@@ -302,12 +310,20 @@ class TwoLevelPreconditioner:
             d.b0_perm = arr(T.perm, np.int32, i32)
             d.b0_panel = T.P
             d.b0_npanel = T.K
-            d.b0_dinv = arr(T.dinv, np.float64, f64)
             d.b0_tile_ptr = arr(T.tile_ptr, np.int64, i64)
             d.b0_tile_col = arr(T.tile_col if T.tile_col.size else np.zeros(1), np.int32, i32)
             d.b0_ntile = int(T.tile_col.size)
-            d.b0_tiles = arr(T.tiles if T.tiles.size else np.zeros(1), np.float64, f64)
             d.b0_ctas = int(os.environ.get("HG_B0_CTAS", "0"))
+            self.b0_mode = mode
+            if mode == 1:
+                d.b0_mode, d.b0_cluster, d.b0_ring = 1, cs, ring
+                dinv = swizzle_tile_rows(T.dinv)
+                tiles = swizzle_tile_rows(T.tiles) if T.tiles.size else np.zeros(1)
+            else:
+                d.b0_mode, d.b0_cluster, d.b0_ring = 0, 0, 0
+                dinv, tiles = T.dinv, (T.tiles if T.tiles.size else np.zeros(1))
+            d.b0_dinv = arr(dinv, np.float64, f64)
+            d.b0_tiles = arr(tiles, np.float64, f64)
         h = ctypes.c_void_p()
         _lib.check(lib.hg_precond_create(ctypes.byref(d), ctypes.byref(h)), "hg_precond_create")
         self._handle = h
