@@ -75,18 +75,37 @@ struct HgOp {
   Workspace ws;
 };
 
+// True under CUDA tool injection (Nsight Compute, compute-sanitizer set
+// CUDA_INJECTION64_PATH), with CUDA_LAUNCH_BLOCKING=1, or HG_SERIAL_APPLY=1.
+static bool serial_kernels() {
+  static const bool s = [] {
+    const char* a = getenv("CUDA_INJECTION64_PATH");
+    const char* b = getenv("CUDA_LAUNCH_BLOCKING");
+    const char* c = getenv("HG_SERIAL_APPLY");
+    return (a && *a) || (b && b[0] == '1') || (c && c[0] == '1');
+  }();
+  return s;
+}
+
 static int precond_apply_core(HgPrecond* P, const double* r, double* out, const double* W, long long ldw,
                               int nv, double* partials, int* nb, cudaStream_t st) {
   if (P->m > 0) {
-    // The latency-bound coarse solve is launched FIRST (side stream) so that
-    // it holds its SMs before the local solves fill the GPU; it starts its
-    // work when this apply's Z^T r chunks are all counted (device-side wait).
     HG_CUDA_TRY(cudaEventRecord(P->ev_fork, st));
     HG_CUDA_TRY(cudaStreamWaitEvent(P->aux, P->ev_fork, 0));
-    HG_TRY(launch_coarse_solve(P, P->aux, P->zt_epoch + (unsigned long long)P->n_zt_items));
+    if (serial_kernels()) {
+      // tools that serialise kernels (profilers, sanitizers, blocking launches):
+      // no kernel may wait on a later one
+      HG_TRY(launch_zt(P, r, P->aux));
+      HG_TRY(launch_coarse_solve(P, P->aux, P->zt_epoch));
+    } else {
+      // The latency-bound coarse solve is launched FIRST (side stream) so that
+      // it holds its SMs before the local solves fill the GPU; it starts its
+      // work when this apply's Z^T r chunks are all counted (device-side wait).
+      HG_TRY(launch_coarse_solve(P, P->aux, P->zt_epoch + (unsigned long long)P->n_zt_items));
+    }
     HG_TRY(launch_zy(P, P->aux));
     HG_CUDA_TRY(cudaEventRecord(P->ev_join, P->aux));
-    HG_TRY(launch_zt(P, r, st));
+    if (!serial_kernels()) HG_TRY(launch_zt(P, r, st));
   }
   HG_TRY(launch_local_solve(P, r, st));
   if (P->m > 0) HG_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_join, 0));
