@@ -75,14 +75,21 @@ struct HgOp {
   Workspace ws;
 };
 
-// True under CUDA tool injection (Nsight Compute, compute-sanitizer set
-// CUDA_INJECTION64_PATH), with CUDA_LAUNCH_BLOCKING=1, or HG_SERIAL_APPLY=1.
+// True under CUDA tool injection (Nsight Compute sets NV_NSIGHT_INJECTION_*,
+// the sanitizer NV_SANITIZER_*, others CUDA_INJECTION64_PATH), with
+// CUDA_LAUNCH_BLOCKING=1, or HG_SERIAL_APPLY=1: such tools serialise kernels.
+extern "C" char** environ;
 static bool serial_kernels() {
   static const bool s = [] {
-    const char* a = getenv("CUDA_INJECTION64_PATH");
     const char* b = getenv("CUDA_LAUNCH_BLOCKING");
     const char* c = getenv("HG_SERIAL_APPLY");
-    return (a && *a) || (b && b[0] == '1') || (c && c[0] == '1');
+    if ((b && b[0] == '1') || (c && c[0] == '1')) return true;
+    for (char** e = environ; e && *e; ++e) {
+      if (!strncmp(*e, "NV_NSIGHT_INJECTION", 19) || !strncmp(*e, "NV_SANITIZER", 12) ||
+          !strncmp(*e, "CUDA_INJECTION64_PATH=", 22) || !strncmp(*e, "NV_TPS_LAUNCH_TOKEN", 19))
+        return true;
+    }
+    return false;
   }();
   return s;
 }
