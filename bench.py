@@ -3,23 +3,34 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 5-16]
 
-A step is one preconditioned solve of one right-hand side of the workload
-(rhs_p = M^{-1} f, then full D_k-weighted GMRES to rtol 1e-6 from x0 = 0,
-exactly cli.run_single's solve block, cli.py:297-307).  The workload is
-BASELINE config 5 at 16x16 subdomains (the north star's ~1M-dof k=100
-config): n = 1024 (1,046,529 dofs), k = 100, a(x) log-uniform [1, 10] on
-64x64 cells (seed 5), overlap 4, cap 60 modes per subdomain (m = 15,360),
-right-hand sides = the config's 16 seeded N(0,1) load vectors.
+The workload is BASELINE config 5 at 16x16 subdomains (the north star's
+~1M-dof k=100 config): n = 1024 (1,046,529 dofs), k = 100, a(x) log-uniform
+[1, 10] on 64x64 cells (seed 5), overlap 4, cap 60 modes per subdomain
+(m = 15,360), right-hand sides = the config's 16 seeded N(0,1) load vectors.
+Config 5 asks for those 16 solved "both one at a time and as a multi-RHS
+block"; both are measured:
 
-value   = GMRES iterations/s over the whole job, inputs resident in HBM
-e2e     = the same metric through the C ABI hg_solve_host with host buffers
-          (H2D of f and D2H of x inside the timed region)
-roofline= the dominant kernel of the apply, timed live with CUDA events
+  step (headline) = the 16-RHS block: R_p = M^{-1} F (one batched apply),
+          then 16 independent full D_k-weighted GMRES solves to rtol 1e-6
+          from x0 = 0 advanced in lock step through shared batched operator
+          applies (hg_gmres_batch) — cli.run_single's solve block
+          (cli.py:297-307) for every column;
+  single_rhs = the same solve one right-hand side at a time (hg_gmres).
+
+value   = GMRES iterations/s (summed over columns) of the block, whole job,
+          inputs resident in HBM
+e2e     = the same metric through the C ABI hg_solve_host_batch with host
+          buffers (H2D of F and D2H of X inside the timed region)
+roofline= the dominant kernel of the step, its time measured live inside
+          the timed region (CUDA events on its stream, hg_stats_*)
 cpu_baseline = the CPU oracle (oracle/, a restatement of the reference's
           SuperLU / LAPACK / numpy solve path) on a bounded sample.
 
-Multi-GPU: one process per GPU (torchrun); ranks solve disjoint right-hand
-sides (weak scaling, no data-path collective); time = max over ranks.
+Multi-GPU: one process per GPU (torchrun); every rank solves the 16-RHS
+block on its own replica of the preconditioner (replicas only: the solve
+phase has no exchange step on one GPU's worth of work), the single-RHS leg
+shards the columns disjointly; no data-path collective (weak scaling);
+time = max over ranks.
 ``--impl reference`` times the CPU oracle port on rank 0 only.
 """
 
@@ -49,6 +60,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cstab", default="cache", help="'cache' (recorded setup constant), 'auto' (recompute)")
+    ap.add_argument("--orth", default="dcgs2", choices=["dcgs2", "measured"])
+    ap.add_argument("--single-steps", type=int, default=3, help="one-at-a-time solves timed for single_rhs")
     return ap.parse_args()
 
 
@@ -156,15 +169,55 @@ def stage_bytes(pre):
     return {"zt": zt, "b0_solve": b0, "zy": zy, "local": loc, "assemble": asm}
 
 
-def solve_bytes(pre, nnz, iters):
-    """Algorithmic bytes of one solve of `iters` iterations (SURVEY §8d model)."""
+def spmv_bytes(n, nnz, ncols=1):
+    """B or D_k applied to ncols vectors: CSR read once, x read + y written per column."""
+    return 12 * nnz + 4 * (n + 1) + 16 * n * ncols
+
+
+def multi_stage_bytes(pre, nr):
+    """Algorithmic bytes of one batched apply of nr columns (factors, Z and
+    B0 streamed once; vector traffic per column)."""
+    nloc = pre.local_sizes
+    loc = sum(8 * n * (kl + kv + 1) + 4 * n + 4 * n for n, (kl, kv) in zip(nloc, pre.local_bands))
+    loc += nr * sum(16 * n for n in nloc)  # gather r + write x_s per column
+    zt = zy = b0 = 0
+    if pre.has_coarse:
+        zt = sum(8 * n * m + 4 * n + 8 * n * nr for n, m in pre.cblock_shapes)
+        zy = sum(8 * n * m + 8 * n * nr for n, m in pre.cblock_shapes) + 8 * pre.m * nr
+        b0 = pre.b0_bytes
+    asm = nr * (8 * sum(nloc) + (8 * sum(n for n, _ in pre.cblock_shapes) if pre.has_coarse else 0) + 8 * pre.n)
+    return {"zt": zt, "b0_solve": b0, "zy": zy, "local": loc, "assemble": asm}
+
+
+def dcgs2_iter_bytes(n, j, ncols):
+    """Arnoldi bytes of DCGS2 iteration j (hg_api.cu gmres_dcgs2) per kernel:
+    dots2 reads Q_{0:j} + (W q_j, W w) per column; the update reads Q_{0:j-1}
+    and rewrites q_j, w; append reads w, ww and writes q_{j+1}, W q_{j+1}."""
+    return {"dots2": ncols * (8 * (j + 1) * n + 16 * n),
+            "update": ncols * (8 * j * n + 32 * n),
+            "append": ncols * 32 * n}
+
+
+def solve_bytes_dcgs2(pre, nnz, iters_per_col, batched):
+    """Algorithmic bytes of one (batched) DCGS2 solve: per iteration j the op
+    (B SpMV + apply on the whole batch), the W w SpMV, the dots, the update,
+    the W SpMV of the projected vector and the append; plus R_p = M^-1 F and
+    x = Q y.  nr columns are active at iteration j (per-column counts)."""
     n = pre.n
-    s_spmv = 12 * nnz + 4 * (n + 1) + 16 * n
-    s_apply = sum(stage_bytes(pre).values())
-    total = s_apply  # rhs_p = M^{-1} f
-    for j in range(iters):
-        total += 2 * s_spmv + s_apply + (32 * (j + 1) + 64) * n
-    total += 8 * n * iters  # x = V y
+    ncol = len(iters_per_col)
+    apply_b = sum((multi_stage_bytes(pre, ncol) if batched else stage_bytes(pre)).values())
+    total = apply_b
+    jmax = max(iters_per_col)
+    for j in range(jmax + 1):  # iteration jmax finalises the last column
+        act = sum(1 for m in iters_per_col if m >= j)
+        if act == 0:
+            break
+        total += spmv_bytes(n, nnz, ncol if batched else 1) + apply_b  # op on the whole batch
+        b = dcgs2_iter_bytes(n, j, act)
+        total += b["dots2"] + spmv_bytes(n, nnz, act)  # W w feeding the dots
+        if j < jmax:
+            total += b["update"] + spmv_bytes(n, nnz, act) + b["append"]
+    total += sum(8 * n * m + 16 * n for m in iters_per_col)  # x = Q y
     return total
 
 
@@ -186,6 +239,17 @@ def ncu_traffic(kernel_key):
 
 
 # ---------------------------------------------------------------- arms
+def read_stats(lib):
+    import ctypes
+
+    from paper_2406_06283_b200 import _lib
+
+    ms = np.zeros(_lib.NPHASES)
+    cnt = np.zeros(_lib.NPHASES, dtype=np.int64)
+    lib.hg_stats_read(_lib.ptr(ms, ctypes.c_double), _lib.ptr(cnt, ctypes.c_int64), 1)
+    return dict(zip(_lib.PHASES, ms.tolist())), dict(zip(_lib.PHASES, cnt.tolist()))
+
+
 def run_ours(args, dist):
     import torch
 
@@ -193,6 +257,7 @@ def run_ours(args, dist):
     from paper_2406_06283_b200 import _lib
 
     torch.cuda.set_device(dist.local)
+    lib = _lib.load()
     t0 = time.perf_counter()
     P = hg.build_problem(args.config, cstab=args.cstab, verbose=dist.rank == 0)
     t_setup = time.perf_counter() - t0
@@ -205,43 +270,109 @@ def run_ours(args, dist):
 
     rhs_host = P.rhs if P.rhs.ndim == 2 else P.rhs[:, None]
     nrhs = rhs_host.shape[1]
-    rhs_dev = torch.from_numpy(np.ascontiguousarray(rhs_host.T)).cuda()  # (nrhs, n), resident in HBM
+    F_dev = torch.from_numpy(np.ascontiguousarray(rhs_host.T)).cuda()  # (nrhs, n): column c contiguous, in HBM
     op = pre.as_operator("T")
     Dk = P.forms.dk
     rtol, maxit = P.config.rtol, P.config.maxit
     stream = torch.cuda.current_stream()
+    n, nnz = pre.n, P.forms.helmholtz.nnz
+    peak, peak_src = peaks()
 
-    def solve(col):
-        rhs_p = pre.apply(rhs_dev[col])
-        x, rep = hg.weighted_gmres(op, rhs_p, weight=Dk, rtol=rtol, maxit=maxit)
-        return rep
+    def solve_block():
+        Rp = pre.apply_multi(F_dev)
+        X, reps = hg.weighted_gmres_batch(op, Rp, weight=Dk, rtol=rtol, maxit=maxit, orth=args.orth)
+        return reps
 
+    # ---------------- headline: the 16-RHS block
     for s in range(args.warmup):
-        rep = solve(shard_columns(s, dist.rank, dist.world, nrhs))
-        log("warmup %d: %d iterations, converged=%s" % (s, rep.iterations, rep.converged))
+        reps = solve_block()
+        log("warmup %d: block of %d, iterations %s" % (s, nrhs, [r.iterations for r in reps]))
+        assert all(r.converged for r in reps), "block solve did not converge"
     dist.barrier()
     torch.cuda.synchronize()
-    launches0 = _lib.load().hg_kernel_launches()
+    launches0 = lib.hg_kernel_launches()
+    lib.hg_stats_enable(1)
+    read_stats(lib)
     clocks = ClockSampler(dist.local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters = 0
+    iters, per_col = 0, []
     ev0.record(stream)
     for s in range(args.steps):
-        rep = solve(shard_columns(args.warmup + s, dist.rank, dist.world, nrhs))
-        iters += rep.iterations
+        reps = solve_block()
+        its = [r.iterations for r in reps]
+        iters += sum(its)
+        per_col.append(its)
     ev1.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
+    phase_ms, phase_cnt = read_stats(lib)
+    lib.hg_stats_enable(0)
     dist.barrier()
-    launches = int(_lib.load().hg_kernel_launches() - launches0)
+    launches = int(lib.hg_kernel_launches() - launches0)
     ms_local = ev0.elapsed_time(ev1)
     ms = dist.max(ms_local)
-    iters_all = dist.sum(iters)
-    value = iters_all / (ms / 1e3)
+    value = dist.sum(iters) / (ms / 1e3)
 
-    # applies/s (device-resident input), its stage profile and the kernel roofline
-    r = rhs_dev[0]
-    out = torch.empty_like(r)
+    # dominant kernel of the step, timed live inside the timed region
+    kb = {"dots2": 0, "update": 0}
+    for its in per_col:
+        jmax = max(its)
+        for j in range(jmax + 1):
+            act = sum(1 for m in its if m >= j)
+            b = dcgs2_iter_bytes(n, j, act)
+            kb["dots2"] += b["dots2"]
+            if j < jmax:
+                kb["update"] += b["update"]
+    cand = {"k_dots2_batch": (phase_ms["proj_dots"], kb["dots2"]), "k_dcgs2_update": (phase_ms["cgs_update"], kb["update"])}
+    dom = max(cand, key=lambda k: cand[k][0])
+    dms, dbytes = cand[dom]
+    launches_dom = phase_cnt["proj_dots" if dom == "k_dots2_batch" else "cgs_update"]
+    ach = dbytes / (dms / 1e3) / 1e9 if dms > 0 else None
+    roofline = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1) if ach else None, "peak": peak,
+                "unit": "GB/s", "frac": round(ach / peak, 4) if ach else None, "traffic": ncu_traffic(dom),
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": int(dbytes / max(launches_dom, 1)),
+                "ms_per_launch": round(dms / max(launches_dom, 1), 4), "launches": launches_dom,
+                "share_of_step": round(dms / ms_local, 4),
+                "phases_ms": {k: round(v, 1) for k, v in phase_ms.items()}}
+    step_ms = ms_local / max(args.steps, 1)
+    sbytes = [solve_bytes_dcgs2(pre, nnz, its, True) for its in per_col] if args.orth == "dcgs2" else None
+    solve_roof = None
+    if sbytes:
+        sb = float(np.mean(sbytes))
+        solve_roof = {"bytes_per_step": int(sb), "achieved": round(sb / (step_ms / 1e3) / 1e9, 1),
+                      "frac": round(sb / (step_ms / 1e3) / 1e9 / peak, 4), "unit": "GB/s",
+                      "model": "bench.solve_bytes_dcgs2 (DESIGN.md section 5)"}
+
+    # ---------------- one right-hand side at a time (same columns)
+    single = None
+    if args.single_steps > 0:
+        def solve_one(col):
+            rhs_p = pre.apply(F_dev[col])
+            x, rep = hg.weighted_gmres(op, rhs_p, weight=Dk, rtol=rtol, maxit=maxit, orth=args.orth)
+            return rep
+
+        solve_one(0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        it1, its1 = 0, []
+        e0.record(stream)
+        for s in range(args.single_steps):
+            rep = solve_one(shard_columns(s, dist.rank, dist.world, nrhs))
+            it1 += rep.iterations
+            its1.append(rep.iterations)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms1 = e0.elapsed_time(e1)
+        sb1 = float(np.mean([solve_bytes_dcgs2(pre, nnz, [m], False) for m in its1])) if args.orth == "dcgs2" else None
+        single = {"value": round(it1 / (ms1 / 1e3), 3), "unit": "iters/s", "solves": args.single_steps,
+                  "iters_per_solve": round(it1 / args.single_steps, 2),
+                  "ms_per_solve": round(ms1 / args.single_steps, 3)}
+        if sb1:
+            single["solve_roofline"] = {"bytes_per_solve": int(sb1),
+                                        "frac": round(sb1 / (ms1 / args.single_steps / 1e3) / 1e9 / peak, 4)}
+
+    # ---------------- applies/s and the serialised stage profiles
+    r = F_dev[0]
     for _ in range(3):
         pre.apply(r)
     torch.cuda.synchronize()
@@ -253,48 +384,44 @@ def run_ours(args, dist):
     e1.record(stream)
     torch.cuda.synchronize()
     apply_ms = e0.elapsed_time(e1) / na
+    e0.record(stream)
+    for _ in range(5):
+        pre.apply_multi(F_dev)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    apply_multi_ms = e0.elapsed_time(e1) / 5
     stages = pre.profile(r, iters=5)
     sb = stage_bytes(pre)
-    peak, peak_src = peaks()
-    dom = max(stages, key=lambda k: stages[k])
-    kern = {"local": "k_local_solve", "b0_solve": "k_b0_solve", "zt": "k_zt", "zy": "k_zy", "assemble": "k_assemble"}
-    ach = sb[dom] / (stages[dom] / 1e3) / 1e9
-    roofline = {"kernel": kern[dom], "bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(ach / peak, 4), "traffic": ncu_traffic(kern[dom]), "peak_source": peak_src,
-                "algorithmic_bytes": sb[dom], "ms": round(stages[dom], 4)}
     per_stage = {k: {"ms": round(stages[k], 4), "bytes": sb[k],
                      "GBps": round(sb[k] / max(stages[k], 1e-9) / 1e6, 1)} for k in stages}
-    it_per_solve = iters / max(args.steps, 1)
-    sbytes = solve_bytes(pre, P.forms.helmholtz.nnz, int(round(it_per_solve)))
-    solve_ms = ms_local / max(args.steps, 1)
-    solve_roof = {"bytes_per_solve": sbytes, "achieved": round(sbytes / (solve_ms / 1e3) / 1e9, 1),
-                  "frac": round(sbytes / (solve_ms / 1e3) / 1e9 / peak, 4), "unit": "GB/s"}
+    stages_m = pre.profile_multi(F_dev, iters=3)
+    sbm = multi_stage_bytes(pre, nrhs)
+    per_stage_m = {k: {"ms": round(stages_m[k], 4), "bytes": sbm[k],
+                       "GBps": round(sbm[k] / max(stages_m[k], 1e-9) / 1e6, 1)} for k in stages_m}
 
-    # e2e through the C ABI with host buffers
+    # ---------------- e2e through the C ABI with host buffers
     e2e = None
     if not args.no_e2e:
-        fh = torch.from_numpy(np.ascontiguousarray(rhs_host[:, 0])).pin_memory().numpy()
-        pre.solve_host(fh, rtol=rtol, maxit=maxit)
+        Fh = torch.from_numpy(np.ascontiguousarray(rhs_host)).pin_memory().numpy()
+        pre.solve_host_batch(Fh, rtol=rtol, maxit=maxit)
         torch.cuda.synchronize()
         dist.barrier()
         e0.record(stream)
         it_e2e = 0
         for s in range(args.steps):
-            col = shard_columns(args.warmup + s, dist.rank, dist.world, nrhs)
-            fh = torch.from_numpy(np.ascontiguousarray(rhs_host[:, col])).pin_memory().numpy()
-            x, rep = pre.solve_host(fh, rtol=rtol, maxit=maxit)
-            it_e2e += rep.iterations
+            X, reps = pre.solve_host_batch(Fh, rtol=rtol, maxit=maxit)
+            it_e2e += sum(r.iterations for r in reps)
         e1.record(stream)
         torch.cuda.synchronize()
         ms_e2e = dist.max(e0.elapsed_time(e1))
         e2e = {"value": round(dist.sum(it_e2e) / (ms_e2e / 1e3), 3), "unit": "iters/s",
-               "h2d_bytes_per_step": 8 * pre.n, "d2h_bytes_per_step": 8 * pre.n + 8 * (maxit + 1),
-               "path": "hg_solve_host (C ABI, host f in, host x out)"}
+               "h2d_bytes_per_step": 8 * n * nrhs, "d2h_bytes_per_step": 8 * n * nrhs + 8 * (maxit + 1) * nrhs,
+               "path": "hg_solve_host_batch (C ABI, host F in, host X out)"}
 
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(P, pre, args.cpu_iters)
-    n = pre.n
+    it_per_solve = iters / max(args.steps, 1) / nrhs
     line = {
         "metric": "GMRES iters/s (FP64, two-level Schwarz + H_k-GenEO, D_k-weighted)",
         "value": round(value, 3),
@@ -310,18 +437,25 @@ def run_ours(args, dist):
         "data": "synthetic, seeded (coefficient seed %d, rhs seeds %d+c)" % (P.config.coeff_seed, P.config.rhs_seed),
         "config": {
             "workload": "BASELINE config %s: n=%d (%d dofs), k=%g, %dx%d subdomains, overlap %d, cap %d (m=%d), "
-                        "a log-uniform[%g,%g] on %dx%d cells" % (
+                        "a log-uniform[%g,%g] on %dx%d cells, %d seeded N(0,1) right-hand sides" % (
                             P.config.name, P.config.n, n, P.config.k, P.config.M, P.config.M, P.config.layers,
                             P.config.cap, pre.m, P.config.coeff_lo, P.config.coeff_hi, P.config.coeff_cells,
-                            P.config.coeff_cells),
-            "step": "rhs_p = M^-1 f; full weighted GMRES to rtol %g from x0=0 (one rhs per rank per step)" % rtol,
-            "l2": "inputs larger than L2: %.2f GB device-resident factors/Z/B0 vs 126 MB L2" % (pre.device_bytes / 1e9),
+                            P.config.coeff_cells, nrhs),
+            "step": "the %d-RHS block: R_p = M^-1 F (batched apply), then %d independent full weighted GMRES "
+                    "solves to rtol %g from x0=0 in lock step (hg_gmres_batch, orth=%s)" % (nrhs, nrhs, rtol, args.orth),
+            "l2": "inputs larger than L2: %.2f GB device-resident factors/Z/B0 + the Krylov bases vs 126 MB L2"
+                  % (pre.device_bytes / 1e9),
             "iters_per_solve": round(it_per_solve, 2),
+            "iters_per_column": per_col[-1],
             "parallelism": "rhs-parallel replicas x%d" % dist.world,
         },
+        "single_rhs": single,
         "applies_per_s": round(1e3 / apply_ms, 2),
         "apply_ms": round(apply_ms, 4),
+        "apply_multi_ms": round(apply_multi_ms, 4),
+        "column_applies_per_s_batched": round(nrhs * 1e3 / apply_multi_ms, 2),
         "stage_ms_serialised": per_stage,
+        "stage_ms_serialised_multi": per_stage_m,
         "solve_roofline": solve_roof,
         "roofline": roofline,
         "setup_s": {k: round(v, 2) for k, v in setup.items()},

@@ -27,6 +27,18 @@
  *   hg_solve_host       <- the solve block of cli.run_single
  *                          (cli.py:297-307): rhs_p = M^{-1} f,
  *                          x = weighted_gmres(M^{-1} B, rhs_p, weight=D_k)
+ *   hg_precond_apply_multi, hg_op_apply_multi, hg_gmres_batch,
+ *   hg_solve_host_batch <- no reference function: the
+ *                          reference solves config 5's 16 right-hand sides
+ *                          one at a time; these run nrhs independent solves
+ *                          (own Krylov space, own stopping test per column)
+ *                          through shared operator applies, so the factors,
+ *                          Z and B0 stream from HBM once per batched apply.
+ *                          Column c of a batch is parity-checked against the
+ *                          one-at-a-time call.
+ *
+ * Batches: nrhs <= HG_MAX_RHS vectors of length n; column c of a batch X
+ * with leading dimension ldx is X + c * ldx (ldx >= n).
  *
  * Threading: a handle is used from one host thread at a time (the reference
  * loop is single threaded).  Results are bitwise deterministic
@@ -49,7 +61,11 @@ extern "C" {
 #define HG_ERR_UNSUPPORTED 3
 #define HG_ERR_NOMEM 4
 
-#define HG_ABI_VERSION 1
+#define HG_ABI_VERSION 2
+
+/* Most right-hand sides one batched call handles (BASELINE config 5's
+ * batch of 16 seeded load vectors). */
+#define HG_MAX_RHS 16
 
 typedef struct HgPrecond HgPrecond; /* opaque: device-resident preconditioner */
 typedef struct HgOp HgOp;           /* opaque: device linear operator */
@@ -166,6 +182,15 @@ int hg_local_solve(HgPrecond* p, int s, const double* r_local, double* x_local, 
 int hg_precond_profile(HgPrecond* p, const double* r, double* out, int32_t iters, double* stage_ms,
                        void* stream);
 
+/* OUT[:, c] = M^{-1} R[:, c] for c < nrhs (one batched apply: local solves
+ * with one warp per column on a shared factor stream, Z^T R and Z Y as dense
+ * FP64 tensor-core (DMMA) contractions, one coarse solve for all columns). */
+int hg_precond_apply_multi(HgPrecond* p, const double* R, int64_t ldr, double* OUT, int64_t ldo, int32_t nrhs,
+                           void* stream);
+/* Stage timing of the batched apply (as hg_precond_profile). */
+int hg_precond_profile_multi(HgPrecond* p, const double* R, int64_t ldr, double* OUT, int64_t ldo, int32_t nrhs,
+                             int32_t iters, double* stage_ms, void* stream);
+
 /* ---- operators for GMRES ---- */
 /* General square CSR operator uploaded from host arrays. */
 int hg_op_create_csr(int32_t n, int64_t nnz, const int32_t* indptr, const int32_t* indices,
@@ -176,6 +201,8 @@ int hg_op_create_csr(int32_t n, int64_t nnz, const int32_t* indptr, const int32_
 int hg_op_create_precond(HgPrecond* p, int mode, HgOp** out);
 int hg_op_destroy(HgOp* op);
 int hg_op_apply(HgOp* op, const double* x, double* y, void* stream);
+/* Y[:, c] = op(X[:, c]), c < nrhs (batched SpMM / batched apply). */
+int hg_op_apply_multi(HgOp* op, const double* X, int64_t ldx, double* Y, int64_t ldy, int32_t nrhs, void* stream);
 
 /* ---- weighted GMRES (wgmres.weighted_gmres) ----
  * Full (unrestarted) GMRES on `op` in the <u,v>_W = v^T W u inner product
@@ -186,11 +213,60 @@ int hg_op_apply(HgOp* op, const double* x, double* y, void* stream);
 int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double* x, double rtol,
              int32_t maxit, double* history, int32_t* info, void* stream);
 
+/* nrhs independent weighted GMRES solves (x0 = 0) advanced in lock step:
+ * every iteration applies `op` once to the batch of current Krylov vectors;
+ * orthogonalisation, the measured second pass, Givens rotations and the
+ * stopping test are per column exactly as in hg_gmres; a converged column
+ * drops out of the Arnoldi kernels.  rhs / x: device batches (ldr, ldx).
+ * history: host, nrhs * (maxit+1) doubles (column c at c*(maxit+1));
+ * info: host, nrhs * 4 ints (as hg_gmres, column c at 4c).  The Krylov
+ * bases live in a virtual reservation that is backed by device memory only
+ * as far as the iterations actually reach. */
+int hg_gmres_batch(HgOp* op, HgOp* weight, const double* rhs, int64_t ldr, double* x, int64_t ldx, int32_t nrhs,
+                   double rtol, int32_t maxit, double* history, int32_t* info, void* stream);
+
+/* Orthogonalisation of hg_gmres / hg_gmres_batch (process-wide setting):
+ * HG_ORTH_MEASURED mirrors wgmres.py:130-156 decision for decision — a
+ *   classical pass, the measurement corr = (W V)^T w, and a second pass when
+ *   max|corr| > 1e-12 ||w||_W (at config 5 it fires on ~80% of iterations);
+ * HG_ORTH_DCGS2 (default) always reorthogonalises, one iteration late
+ *   (delayed classical Gram-Schmidt twice): the reorthogonalisation dots of
+ *   q_j share one basis read with the projection dots of A q_j, and the
+ *   correction of q_j shares one basis read with the projection update, so
+ *   an iteration reads the basis twice instead of three to four times.
+ *   Same Krylov space, CGS2-level orthogonality; the parity bars (iterations
+ *   +-1, solution 1e-8) are tested against the reference for both modes. */
+#define HG_ORTH_MEASURED 0
+#define HG_ORTH_DCGS2 1
+int hg_set_orthogonalization(int mode);
+int hg_get_orthogonalization(void);
+
+/* Phase timing of hg_gmres / hg_gmres_batch (measurement hook, used by
+ * bench.py to time kernels live inside its timed region).  While enabled,
+ * each phase of each iteration is bracketed by CUDA events on the solve's
+ * stream; the elapsed device times are summed when the solve synchronises.
+ * Phases: 0 operator apply (B SpMV + preconditioner, with the fused
+ * projection dots of the single-RHS measured path), 1 projection dots
+ * h = (W V)^T w, 2 CGS update w -= V h, 3 measurement (corr dots + W SpMV +
+ * norm), 4 second pass, 5 append V_{j+1}, W V_{j+1}, 6 the W w SpMV feeding
+ * the dots.  In DCGS2 mode 1 = the fused reorthogonalisation/projection dots
+ * (k_dots2_batch + its reduction), 2 = the fused update (k_dcgs2_update),
+ * 3 = W SpMV + norm of the projected vector, 4 unused. */
+#define HG_NPHASES 7
+int hg_stats_enable(int on);
+/* ms, count: host arrays of HG_NPHASES; reset != 0 clears the accumulators. */
+int hg_stats_read(double* ms, int64_t* count, int reset);
+
 /* End-to-end solve with HOST buffers (the drop-in for cli.py:297-307):
  * f (host, n) -> x (host, n); rhs_p = M^{-1} f ; x = GMRES(M^{-1}B, rhs_p,
  * weight D_k).  H2D and D2H copies are inside the call. */
 int hg_solve_host(HgPrecond* p, const double* f_host, double* x_host, double rtol, int32_t maxit,
                   double* history, int32_t* info, void* stream);
+
+/* Batched end-to-end solve with HOST buffers: F (host, column c at F + c*n)
+ * -> X (host, same layout); rhs_p = M^{-1} F and the batched GMRES. */
+int hg_solve_host_batch(HgPrecond* p, const double* F_host, double* X_host, int32_t nrhs, double rtol,
+                        int32_t maxit, double* history, int32_t* info, void* stream);
 
 #ifdef __cplusplus
 }

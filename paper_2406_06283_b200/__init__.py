@@ -57,6 +57,6 @@ from .schwarz import (
     TwoLevelPreconditioner,
     factorize,
 )
-from .wgmres import GmresReport, elman_gamma, weighted_gmres
+from .wgmres import GmresReport, elman_gamma, weighted_gmres, weighted_gmres_batch
 
 __version__ = "0.1.0"

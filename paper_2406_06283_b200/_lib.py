@@ -91,7 +91,32 @@ SIGNATURES = {
         ctypes.c_int,
         [_vp, _f64p, _f64p, ctypes.c_double, ctypes.c_int32, _f64p, _i32p, _vp],
     ),
+    "hg_precond_apply_multi": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int32, _vp]),
+    "hg_precond_profile_multi": (
+        ctypes.c_int,
+        [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _f64p, _vp],
+    ),
+    "hg_op_apply_multi": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int32, _vp]),
+    "hg_gmres_batch": (
+        ctypes.c_int,
+        [_vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_int32,
+         _f64p, _i32p, _vp],
+    ),
+    "hg_solve_host_batch": (
+        ctypes.c_int,
+        [_vp, _f64p, _f64p, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, _f64p, _i32p, _vp],
+    ),
+    "hg_stats_enable": (ctypes.c_int, [ctypes.c_int]),
+    "hg_set_orthogonalization": (ctypes.c_int, [ctypes.c_int]),
+    "hg_get_orthogonalization": (ctypes.c_int, []),
+    "hg_stats_read": (ctypes.c_int, [_f64p, _i64p, ctypes.c_int]),
 }
+
+ABI_VERSION = 2
+NPHASES = 6
+ORTH = {"measured": 0, "dcgs2": 1}
+PHASES = ("op_apply", "proj_dots", "cgs_update", "measure", "second_pass", "append")
+MAX_RHS = 16
 
 _LIB = None
 
@@ -111,7 +136,7 @@ def load(path=LIB_PATH):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.hg_abi_version() != 1:
+    if lib.hg_abi_version() != ABI_VERSION:
         raise ImportError("libhelmgpu.so ABI mismatch")
     if path == LIB_PATH:
         _LIB = lib

@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "hg_internal.cuh"
 
 namespace hg {
@@ -66,6 +68,212 @@ struct Workspace {
   }
 };
 
+// Device memory that grows on demand inside one virtual reservation (CUDA
+// VMM): the batched Krylov bases are reserved for maxit+1 vectors per column
+// (up to ~270 GB of address space at config 5) but backed by HBM only as far
+// as the iterations reach, so 16 full-GMRES bases fit the 180 GB device.
+struct VmBuf {
+  CUdeviceptr base = 0;
+  size_t reserved = 0, mapped = 0, gran = 0;
+  std::vector<CUmemGenericAllocationHandle> handles;
+  std::vector<size_t> sizes;
+  int dev = 0;
+  double* ptr() const { return reinterpret_cast<double*>(base); }
+  int reserve(size_t bytes);
+  int ensure(size_t bytes);
+  void free_all();
+  ~VmBuf() { free_all(); }
+};
+
+struct DrvApi {
+  decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+  decltype(&cuMemAddressReserve) reserve = nullptr;
+  decltype(&cuMemAddressFree) addr_free = nullptr;
+  decltype(&cuMemCreate) create = nullptr;
+  decltype(&cuMemRelease) release = nullptr;
+  decltype(&cuMemMap) map = nullptr;
+  decltype(&cuMemUnmap) unmap = nullptr;
+  decltype(&cuMemSetAccess) set_access = nullptr;
+  bool ok = false;
+};
+
+static const DrvApi& drv() {
+  static DrvApi d = [] {
+    DrvApi a;
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess && *fn != nullptr;
+    };
+    a.ok = get("cuMemGetAllocationGranularity", reinterpret_cast<void**>(&a.granularity)) &&
+           get("cuMemAddressReserve", reinterpret_cast<void**>(&a.reserve)) &&
+           get("cuMemAddressFree", reinterpret_cast<void**>(&a.addr_free)) &&
+           get("cuMemCreate", reinterpret_cast<void**>(&a.create)) &&
+           get("cuMemRelease", reinterpret_cast<void**>(&a.release)) &&
+           get("cuMemMap", reinterpret_cast<void**>(&a.map)) &&
+           get("cuMemUnmap", reinterpret_cast<void**>(&a.unmap)) &&
+           get("cuMemSetAccess", reinterpret_cast<void**>(&a.set_access));
+    return a;
+  }();
+  return d;
+}
+
+static CUmemAllocationProp vm_prop(int dev) {
+  CUmemAllocationProp p = {};
+  p.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  p.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  p.location.id = dev;
+  return p;
+}
+
+int VmBuf::reserve(size_t bytes) {
+  free_all();
+  const DrvApi& d = drv();
+  if (!d.ok) {
+    set_error("CUDA virtual memory management entry points unavailable");
+    return HG_ERR_UNSUPPORTED;
+  }
+  HG_CUDA_TRY(cudaGetDevice(&dev));
+  CUmemAllocationProp p = vm_prop(dev);
+  if (d.granularity(&gran, &p, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || gran == 0) {
+    set_error("cuMemGetAllocationGranularity failed");
+    return HG_ERR_CUDA;
+  }
+  reserved = (bytes + gran - 1) / gran * gran;
+  if (d.reserve(&base, reserved, 0, 0, 0) != CUDA_SUCCESS) {
+    base = 0;
+    reserved = 0;
+    set_error("cuMemAddressReserve failed");
+    return HG_ERR_NOMEM;
+  }
+  return HG_OK;
+}
+
+int VmBuf::ensure(size_t bytes) {
+  if (bytes <= mapped) return HG_OK;
+  if (bytes > reserved) {
+    set_error("VmBuf: request beyond the reservation");
+    return HG_ERR_ARG;
+  }
+  const DrvApi& d = drv();
+  const size_t chunk_min = (std::max<size_t>((size_t)256 << 20, reserved / 16) + gran - 1) / gran * gran;
+  while (mapped < bytes) {
+    size_t sz = std::max(chunk_min, (bytes - mapped + gran - 1) / gran * gran);
+    sz = std::min(sz, reserved - mapped);
+    CUmemAllocationProp p = vm_prop(dev);
+    CUmemGenericAllocationHandle h;
+    if (d.create(&h, sz, &p, 0) != CUDA_SUCCESS) {
+      set_error("cuMemCreate failed (device memory exhausted by the Krylov bases?)");
+      return HG_ERR_NOMEM;
+    }
+    if (d.map(base + mapped, sz, 0, h, 0) != CUDA_SUCCESS) {
+      d.release(h);
+      set_error("cuMemMap failed");
+      return HG_ERR_CUDA;
+    }
+    CUmemAccessDesc acc = {};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = dev;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if (d.set_access(base + mapped, sz, &acc, 1) != CUDA_SUCCESS) {
+      d.unmap(base + mapped, sz);
+      d.release(h);
+      set_error("cuMemSetAccess failed");
+      return HG_ERR_CUDA;
+    }
+    handles.push_back(h);
+    sizes.push_back(sz);
+    mapped += sz;
+  }
+  return HG_OK;
+}
+
+void VmBuf::free_all() {
+  if (!base) return;
+  const DrvApi& d = drv();
+  cudaDeviceSynchronize();
+  size_t off = 0;
+  for (size_t i = 0; i < handles.size(); ++i) {
+    d.unmap(base + off, sizes[i]);
+    d.release(handles[i]);
+    off += sizes[i];
+  }
+  d.addr_free(base, reserved);
+  handles.clear();
+  sizes.clear();
+  base = 0;
+  reserved = mapped = 0;
+}
+
+// Batched GMRES workspace.  Basis layout [i][c][n]: vector i of column c at
+// V + (i * nrhs + c) * n, so the op input of iteration j is one contiguous
+// batch (ld n) and the bases grow contiguously.
+struct BatchWs {
+  int n = 0, nrhs = 0, cap = 0;
+  bool weighted = false;
+  VmBuf V, WV;
+  double* w = nullptr;          // [c][n] op output / Krylov candidate
+  double* ww = nullptr;         // [c][n] W w
+  double* partials = nullptr;   // [c][nb][cap + 2]
+  double* pself = nullptr;      // [c][nb] self-dot partials of the weight SpMM
+  double* dh = nullptr;         // [c][cap + 2]
+  double* dc = nullptr;         // [c][cap + 2]
+  double* dy = nullptr;         // [c][cap + 2]
+  double* hbuf = nullptr;       // pinned [2][c][cap + 2]
+  ~BatchWs() { clear(); }
+  void clear() {
+    release(w);
+    release(ww);
+    release(partials);
+    release(pself);
+    release(dh);
+    release(dc);
+    release(dy);
+    if (hbuf) cudaFreeHost(hbuf);
+    hbuf = nullptr;
+    V.free_all();
+    WV.free_all();
+    n = nrhs = cap = 0;
+  }
+};
+
+// DCGS2 workspace (single and batched solves).  Basis Q as in BatchWs; no
+// cached W Q: the dots read Q against W w (SpMV) and W q_j (kept from the
+// previous normalisation), so the basis costs one vector per iteration.
+struct DcWs {
+  int n = 0, nrhs = 0, cap = 0;
+  bool weighted = false;
+  VmBuf Q;
+  double* w = nullptr;          // [c][n] op output, then the projected vector
+  double* u = nullptr;          // [c][n] W w
+  double* ww = nullptr;         // [c][n] W w after projection
+  double* wq = nullptr;         // [c][n] W q_j (of the not yet reorthogonalised q_j)
+  double* partials = nullptr;   // [c][nb][2 (cap + 2)]
+  double* pself = nullptr;      // [c][nb256]
+  double* dots = nullptr;       // [c][2 (cap + 2)]
+  double* nrm2 = nullptr;       // [c] ||w||_W^2 of the last projected vector
+  double* coef = nullptr;       // [c][2 (cap + 2)] rinv, s, c
+  double* dy = nullptr;         // [c][cap + 2]
+  double* hbuf = nullptr;       // pinned: dots [c][2(cap+2)], nrm2 [c], coef [c][2(cap+2)]
+  ~DcWs() { clear(); }
+  void clear() {
+    release(w);
+    release(u);
+    release(ww);
+    release(wq);
+    release(partials);
+    release(pself);
+    release(dots);
+    release(nrm2);
+    release(coef);
+    release(dy);
+    if (hbuf) cudaFreeHost(hbuf);
+    hbuf = nullptr;
+    Q.free_all();
+    n = nrhs = cap = 0;
+  }
+};
+
 struct HgOp {
   int kind = 0;  // 0: owned CSR; 1: preconditioner-backed
   int n = 0;
@@ -73,7 +281,13 @@ struct HgOp {
   HgPrecond* P = nullptr;
   int mode = 0;
   Workspace ws;
+  BatchWs bws;
+  DcWs dws;    // one right-hand side
+  DcWs dwsb;   // batches
 };
+
+// Orthogonalisation scheme of hg_gmres / hg_gmres_batch (hg_set_orthogonalization).
+static int g_orth = HG_ORTH_DCGS2;
 
 // True under CUDA tool injection (Nsight Compute sets NV_NSIGHT_INJECTION_*,
 // the sanitizer NV_SANITIZER_*, others CUDA_INJECTION64_PATH), with
@@ -93,6 +307,62 @@ static bool serial_kernels() {
   }();
   return s;
 }
+
+// ---- phase timing (hg_stats_*): event pairs per phase, summed at solve end
+namespace {
+struct PhaseStats {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<std::pair<int, size_t>> open;  // (phase, index of the start event)
+  double ms[HG_NPHASES] = {0};
+  long long count[HG_NPHASES] = {0};
+};
+PhaseStats g_stats;
+
+cudaEvent_t stats_event() {
+  if (g_stats.used == g_stats.pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_stats.pool.push_back(e);
+  }
+  return g_stats.pool[g_stats.used++];
+}
+
+// phase bracket: start on construction, stop on destruction (same stream)
+struct Phase {
+  cudaStream_t st;
+  int ph;
+  size_t i0 = 0;
+  bool on;
+  Phase(cudaStream_t s, int p) : st(s), ph(p), on(g_stats.on) {
+    if (on) {
+      i0 = g_stats.used;
+      cudaEventRecord(stats_event(), st);
+    }
+  }
+  ~Phase() {
+    if (on) {
+      cudaEventRecord(stats_event(), st);
+      g_stats.open.emplace_back(ph, i0);
+    }
+  }
+};
+
+// called after the solve's final synchronisation
+void stats_collect() {
+  if (!g_stats.on) return;
+  for (auto& pr : g_stats.open) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, g_stats.pool[pr.second], g_stats.pool[pr.second + 1]) == cudaSuccess) {
+      g_stats.ms[pr.first] += t;
+      g_stats.count[pr.first] += 1;
+    }
+  }
+  g_stats.open.clear();
+  g_stats.used = 0;
+}
+}  // namespace
 
 static int precond_apply_core(HgPrecond* P, const double* r, double* out, const double* W, long long ldw,
                               int nv, double* partials, int* nb, cudaStream_t st) {
@@ -150,6 +420,60 @@ static int op_apply_dots(HgOp* op, const double* x, double* y, const double* W, 
   }
 }
 
+static int precond_apply_multi_core(HgPrecond* P, const double* R, long long ldr, double* OUT, long long ldo,
+                                    int nrhs, cudaStream_t st) {
+  if (nrhs < 1 || nrhs > HG_MAX_RHS) {
+    set_error("batched apply: nrhs must be in [1, HG_MAX_RHS]");
+    return HG_ERR_ARG;
+  }
+  HG_TRY(multi_prepare(P));
+  if (P->m > 0) {
+    HG_CUDA_TRY(cudaEventRecord(P->ev_fork, st));
+    HG_CUDA_TRY(cudaStreamWaitEvent(P->aux, P->ev_fork, 0));
+    if (serial_kernels()) {
+      HG_TRY(launch_zt_multi(P, R, ldr, nrhs, P->aux));
+      HG_TRY(launch_b0_multi(P, nrhs, P->aux, P->zt_epoch));
+    } else {
+      // as the single-RHS apply: the persistent coarse solve first (holds its
+      // SMs), released by the Z^T R chunk counter
+      HG_TRY(launch_b0_multi(P, nrhs, P->aux, P->zt_epoch + (unsigned long long)P->n_zt_items));
+    }
+    HG_TRY(launch_zy_multi(P, nrhs, P->aux));
+    HG_CUDA_TRY(cudaEventRecord(P->ev_join, P->aux));
+    if (!serial_kernels()) HG_TRY(launch_zt_multi(P, R, ldr, nrhs, st));
+  }
+  HG_TRY(launch_local_solve_multi(P, R, ldr, nrhs, st));
+  if (P->m > 0) HG_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_join, 0));
+  return launch_assemble_multi(P, true, true, OUT, ldo, nrhs, st);
+}
+
+// Y[:, c] = op(X[:, c])
+static int op_apply_multi(HgOp* op, const double* X, long long ldx, double* Y, long long ldy, int nrhs,
+                          cudaStream_t st) {
+  if (op->kind == 0) return launch_spmm(op->csr, op->csr.data, X, ldx, Y, ldy, nrhs, st);
+  HgPrecond* P = op->P;
+  switch (op->mode) {
+    case 0:
+      return precond_apply_multi_core(P, X, ldx, Y, ldy, nrhs, st);
+    case 1:
+      HG_TRY(multi_prepare(P));
+      HG_TRY(launch_spmm(P->A, P->A.data, X, ldx, P->d_tmpm, P->n, nrhs, st));
+      return precond_apply_multi_core(P, P->d_tmpm, P->n, Y, ldy, nrhs, st);
+    case 2:
+    case 3: {
+      const double* vals = op->mode == 2 ? P->A.data : P->A.data2;
+      if (!vals) {
+        set_error("operator needs D_k but the handle was created without it");
+        return HG_ERR_ARG;
+      }
+      return launch_spmm(P->A, vals, X, ldx, Y, ldy, nrhs, st);
+    }
+    default:
+      set_error("bad operator mode");
+      return HG_ERR_ARG;
+  }
+}
+
 // y = W x with fused self dot (x.y) and dots of x against Wb[0..nv)
 static int weight_apply_dots(HgOp* wop, const double* x, double* y, const double* Wb, long long ldw, int nv,
                              double* partials, int* nb, cudaStream_t st) {
@@ -197,6 +521,25 @@ static int ws_reserve(Workspace& ws, int n, int cap, bool weighted) {
 extern "C" {
 
 int hg_abi_version(void) { return HG_ABI_VERSION; }
+
+int hg_stats_enable(int on) {
+  g_stats.on = on != 0;
+  g_stats.open.clear();
+  g_stats.used = 0;
+  return HG_OK;
+}
+
+int hg_stats_read(double* ms, int64_t* count, int reset) {
+  for (int p = 0; p < HG_NPHASES; ++p) {
+    if (ms) ms[p] = g_stats.ms[p];
+    if (count) count[p] = g_stats.count[p];
+    if (reset) {
+      g_stats.ms[p] = 0.0;
+      g_stats.count[p] = 0;
+    }
+  }
+  return HG_OK;
+}
 const char* hg_last_error(void) { return g_err.c_str(); }
 int64_t hg_kernel_launches(void) { return g_launches.load(); }
 int hg_device_sync(void) {
@@ -236,6 +579,13 @@ int hg_precond_destroy(HgPrecond* P) {
   release(P->d_cptr);
   release(P->d_cent);
   release(P->d_tmp);
+  release(P->d_xsm);
+  release(P->d_zsm);
+  release(P->d_cpartm);
+  release(P->d_ym);
+  release(P->d_b0m_x);
+  release(P->d_b0m_done);
+  release(P->d_tmpm);
   if (P->aux) cudaStreamDestroy(P->aux);
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);
   if (P->ev_join) cudaEventDestroy(P->ev_join);
@@ -416,6 +766,9 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
   HG_TRY(preload_assemble());
   HG_TRY(preload_b0());
   HG_TRY(preload_vec());
+  HG_TRY(preload_multi());
+  HG_TRY(preload_dcgs2());
+  HG_TRY(preload_add());
   HG_CUDA_TRY(cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking));
   HG_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
   HG_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
@@ -511,6 +864,55 @@ int hg_precond_profile(HgPrecond* P, const double* r, double* out, int32_t iters
   return status;
 }
 
+int hg_precond_apply_multi(HgPrecond* P, const double* R, int64_t ldr, double* OUT, int64_t ldo, int32_t nrhs,
+                           void* stream) {
+  if (!P || !R || !OUT || ldr < P->n || ldo < P->n) {
+    set_error("hg_precond_apply_multi: bad argument");
+    return HG_ERR_ARG;
+  }
+  return precond_apply_multi_core(P, R, ldr, OUT, ldo, nrhs, (cudaStream_t)stream);
+}
+
+int hg_precond_profile_multi(HgPrecond* P, const double* R, int64_t ldr, double* OUT, int64_t ldo, int32_t nrhs,
+                             int32_t iters, double* stage_ms, void* stream) {
+  if (!P || !R || !OUT || !stage_ms || iters <= 0 || nrhs < 1 || nrhs > HG_MAX_RHS || ldr < P->n || ldo < P->n) {
+    set_error("hg_precond_profile_multi: bad argument");
+    return HG_ERR_ARG;
+  }
+  HG_TRY(multi_prepare(P));
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t ev[HG_NSTAGES + 1];
+  for (auto& e : ev) HG_CUDA_TRY(cudaEventCreate(&e));
+  double acc[HG_NSTAGES] = {0, 0, 0, 0, 0};
+  int status = HG_OK;
+  for (int it = 0; it < iters && status == HG_OK; ++it) {
+    cudaEventRecord(ev[0], st);
+    if ((status = launch_zt_multi(P, R, ldr, nrhs, st)) != HG_OK) break;
+    cudaEventRecord(ev[1], st);
+    if ((status = launch_b0_multi(P, nrhs, st, P->zt_epoch)) != HG_OK) break;
+    cudaEventRecord(ev[2], st);
+    if ((status = launch_zy_multi(P, nrhs, st)) != HG_OK) break;
+    cudaEventRecord(ev[3], st);
+    if ((status = launch_local_solve_multi(P, R, ldr, nrhs, st)) != HG_OK) break;
+    cudaEventRecord(ev[4], st);
+    if ((status = launch_assemble_multi(P, true, true, OUT, ldo, nrhs, st)) != HG_OK) break;
+    cudaEventRecord(ev[5], st);
+    if (cudaEventSynchronize(ev[5]) != cudaSuccess) {
+      set_error("hg_precond_profile_multi: event sync failed");
+      status = HG_ERR_CUDA;
+      break;
+    }
+    for (int s = 0; s < HG_NSTAGES; ++s) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[s], ev[s + 1]);
+      acc[s] += ms;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int s = 0; s < HG_NSTAGES; ++s) stage_ms[s] = acc[s] / iters;
+  return status;
+}
+
 int hg_precond_spmv(HgPrecond* P, int which, const double* x, double* y, void* stream) {
   if (!P || !x || !y || (which != 0 && which != 1)) {
     set_error("hg_precond_spmv: bad argument");
@@ -587,7 +989,18 @@ int hg_op_apply(HgOp* op, const double* x, double* y, void* stream) {
   return op_apply_dots(op, x, y, nullptr, 0, 0, nullptr, nullptr, (cudaStream_t)stream);
 }
 
+int hg_op_apply_multi(HgOp* op, const double* X, int64_t ldx, double* Y, int64_t ldy, int32_t nrhs, void* stream) {
+  if (!op || !X || !Y || nrhs < 1 || nrhs > HG_MAX_RHS || ldx < op->n || ldy < op->n) {
+    set_error("hg_op_apply_multi: bad argument");
+    return HG_ERR_ARG;
+  }
+  return op_apply_multi(op, X, ldx, Y, ldy, nrhs, (cudaStream_t)stream);
+}
+
 // ------------------------------------------------------------------ GMRES
+static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr, double* x, long long ldx, int nrhs,
+                       double rtol, int maxit, double* history, int32_t* info, cudaStream_t st);
+
 // Restates wgmres.weighted_gmres (wgmres.py:74-203): classical Gram-Schmidt
 // with the reference's measured, conditional second pass (the measurement
 // corr = (W V)^T w is always taken, as wgmres.py:142), W-norm via one weight
@@ -606,6 +1019,19 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
   cudaStream_t st = (cudaStream_t)stream;
   const int n = op->n;
   maxit = std::max(0, std::min(maxit, n));
+  if (g_orth == HG_ORTH_DCGS2) {
+    if (!x0) return gmres_dcgs2(op, weight, rhs, n, x, n, 1, rtol, maxit, history, info, st);
+    // r0 = rhs - op(x0); x = x0 + GMRES(r0)
+    double* r0 = nullptr;
+    HG_CUDA_TRY(cudaMallocAsync(&r0, sizeof(double) * n, st));
+    int s = op_apply_dots(op, x0, x, nullptr, 0, 0, nullptr, nullptr, st);
+    if (s == HG_OK) s = launch_sub(n, rhs, x, r0, st);
+    if (s == HG_OK) s = gmres_dcgs2(op, weight, r0, n, x, n, 1, rtol, maxit, history, info, st);
+    if (s == HG_OK) s = launch_add(n, x, x0, x, st);
+    cudaFreeAsync(r0, st);
+    HG_CUDA_TRY(cudaStreamSynchronize(st));
+    return s;
+  }
   Workspace& ws = op->ws;
   const bool weighted = weight != nullptr;
   HG_TRY(ws_reserve(ws, n, maxit + 1, weighted));
@@ -656,17 +1082,26 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
   for (int j = 0; j < maxit; ++j) {
     const int nv = j + 1;
     double* w = ws.w;
-    // w = op(V_j), fused h_i = (W V_i) . w
-    HG_TRY(op_apply_dots(op, V + (long long)j * ld, w, WV, ld, nv, ws.partials, &nb, st));
-    HG_TRY(launch_reduce(ws.partials, nb, nv + 1, ws.dh, st));
-    // classical GS pass: w -= V h
-    HG_TRY(launch_axpy_multi(n, w, V, ld, nv, ws.dh + 1, 1, st));
-    // ww = W w with w.ww and the measurement corr_i = (W V_i) . w
-    if (weighted)
-      HG_TRY(weight_apply_dots(weight, w, ws.ww, WV, ld, nv, ws.partials, &nb, st));
-    else
-      HG_TRY(launch_dots(n, w, V, ld, nv, ws.partials, &nb, st));
-    HG_TRY(launch_reduce(ws.partials, nb, nv + 1, ws.dc, st));
+    {  // w = op(V_j), fused h_i = (W V_i) . w
+      Phase ph(st, 0);
+      HG_TRY(op_apply_dots(op, V + (long long)j * ld, w, WV, ld, nv, ws.partials, &nb, st));
+    }
+    {
+      Phase ph(st, 1);
+      HG_TRY(launch_reduce(ws.partials, nb, nv + 1, ws.dh, st));
+    }
+    {  // classical GS pass: w -= V h
+      Phase ph(st, 2);
+      HG_TRY(launch_axpy_multi(n, w, V, ld, nv, ws.dh + 1, 1, st));
+    }
+    {  // ww = W w with w.ww and the measurement corr_i = (W V_i) . w
+      Phase ph(st, 3);
+      if (weighted)
+        HG_TRY(weight_apply_dots(weight, w, ws.ww, WV, ld, nv, ws.partials, &nb, st));
+      else
+        HG_TRY(launch_dots(n, w, V, ld, nv, ws.partials, &nb, st));
+      HG_TRY(launch_reduce(ws.partials, nb, nv + 1, ws.dc, st));
+    }
     HG_CUDA_TRY(cudaMemcpyAsync(hb, ws.dh + 1, sizeof(double) * nv, cudaMemcpyDeviceToHost, st));
     HG_CUDA_TRY(cudaMemcpyAsync(hb + nv, ws.dc, sizeof(double) * (nv + 1), cudaMemcpyDeviceToHost, st));
     HG_CUDA_TRY(cudaStreamSynchronize(st));
@@ -675,6 +1110,7 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
     double cmax = 0.0;
     for (int i = 0; i < nv; ++i) cmax = std::max(cmax, std::fabs(hb[nv + 1 + i]));
     if (cmax > REORTH_TOL * std::max(hnorm, 1e-300)) {
+      Phase ph(st, 4);
       for (int i = 0; i < nv; ++i) col[i] += hb[nv + 1 + i];
       HG_TRY(launch_axpy_multi(n, w, V, ld, nv, ws.dc + 1, 1, st));
       if (weighted)
@@ -693,6 +1129,7 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
     if (hnorm <= BREAKDOWN_RTOL * std::max(cscale, 1e-300)) {
       breakdown = true;
     } else {
+      Phase ph(st, 5);
       HG_TRY(launch_scale2(n, w, weighted ? ws.ww : w, &hnorm, V + (long long)(j + 1) * ld,
                            weighted ? WV + (long long)(j + 1) * ld : nullptr, st));
     }
@@ -743,10 +1180,29 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
     HG_TRY(launch_fill(n, x, 0.0, st));
   }
   HG_CUDA_TRY(cudaStreamSynchronize(st));
+  stats_collect();
   info[0] = m;
   info[1] = converged ? 1 : 0;
   info[2] = breakdown ? 1 : 0;
   info[3] = reorth;
+  return HG_OK;
+}
+
+static int ensure_solve_ops(HgPrecond* P) {
+  if (!P->op_T) {
+    HgOp* t = new HgOp();
+    t->kind = 1;
+    t->n = P->n;
+    t->P = P;
+    t->mode = 1;
+    HgOp* w = new HgOp();
+    w->kind = 1;
+    w->n = P->n;
+    w->P = P;
+    w->mode = 3;
+    P->op_T = t;
+    P->op_W = w;
+  }
   return HG_OK;
 }
 
@@ -758,20 +1214,7 @@ int hg_solve_host(HgPrecond* P, const double* f_host, double* x_host, double rto
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int n = P->n;
-  if (!P->op_T) {
-    HgOp* t = new HgOp();
-    t->kind = 1;
-    t->n = n;
-    t->P = P;
-    t->mode = 1;
-    HgOp* w = new HgOp();
-    w->kind = 1;
-    w->n = n;
-    w->P = P;
-    w->mode = 3;
-    P->op_T = t;
-    P->op_W = w;
-  }
+  HG_TRY(ensure_solve_ops(P));
   double *d_f = nullptr, *d_rhs = nullptr, *d_x = nullptr;
   HG_CUDA_TRY(cudaMallocAsync(&d_f, sizeof(double) * n, st));
   HG_CUDA_TRY(cudaMallocAsync(&d_rhs, sizeof(double) * n, st));
@@ -791,3 +1234,612 @@ int hg_solve_host(HgPrecond* P, const double* f_host, double* x_host, double rto
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ DCGS2 driver
+// Full weighted GMRES (wgmres.py:74-203 semantics: x0 = 0 here, left
+// operator given, D_k inner product, stop when |g_{j+1}| <= rtol beta or on
+// breakdown, maxit = min(maxit, n)) with delayed classical Gram-Schmidt
+// twice (Hernandez/Swirydowicz-Bielich "DCGS2" Arnoldi):
+//   iteration j:  w = A q_j                              (q_j projected once)
+//                 [s; alpha] = Q_{0:j}^T W q_j, z = Q_{0:j}^T W w   (ONE basis read)
+//                 rho = sqrt(alpha - s.s); column j-1 corrected: H[:j, j-1] += beta s,
+//                 H[j, j-1] = beta rho  -> Givens, history, stopping test on the host
+//                 z'_j = (z_j - s.z)/rho; Hs = H s; h = (z' - Hs)/rho
+//                 q_j <- (q_j - Q s)/rho ; w <- w/rho - Q (Hs/rho + h)   (ONE basis read)
+//                 beta = ||w||_W (W SpMV), q_{j+1} = w/beta on the device.
+// nrhs columns advance in lock step with their own bases and host state;
+// nrhs == 1 runs the single-RHS operator kernels.
+static int dws_reserve(DcWs& ws, int n, int nrhs, int cap, bool weighted) {
+  if (ws.n == n && ws.nrhs == nrhs && ws.cap >= cap && ws.weighted == weighted) return HG_OK;
+  ws.clear();
+  ws.n = n;
+  ws.nrhs = nrhs;
+  ws.cap = cap;
+  ws.weighted = weighted;
+  HG_TRY(ws.Q.reserve(sizeof(double) * (size_t)n * nrhs * cap));
+  const size_t nn = (size_t)n * nrhs;
+  const size_t W2 = 2 * (size_t)(cap + 2);
+  HG_CUDA_TRY(cudaMalloc(&ws.w, sizeof(double) * nn));
+  HG_CUDA_TRY(cudaMalloc(&ws.u, sizeof(double) * nn));
+  HG_CUDA_TRY(cudaMalloc(&ws.ww, sizeof(double) * nn));
+  HG_CUDA_TRY(cudaMalloc(&ws.wq, sizeof(double) * nn));
+  HG_CUDA_TRY(cudaMalloc(&ws.partials, sizeof(double) * (size_t)ceil_div(n, VEC_TILE) * W2 * nrhs));
+  HG_CUDA_TRY(cudaMalloc(&ws.pself, sizeof(double) * (size_t)ceil_div(n, 256) * nrhs));
+  HG_CUDA_TRY(cudaMalloc(&ws.dots, sizeof(double) * W2 * nrhs));
+  HG_CUDA_TRY(cudaMalloc(&ws.nrm2, sizeof(double) * nrhs));
+  HG_CUDA_TRY(cudaMalloc(&ws.coef, sizeof(double) * W2 * nrhs));
+  HG_CUDA_TRY(cudaMalloc(&ws.dy, sizeof(double) * (size_t)(cap + 2) * nrhs));
+  HG_CUDA_TRY(cudaMallocHost(&ws.hbuf, sizeof(double) * (2 * W2 * nrhs + nrhs + (size_t)(cap + 2) * nrhs)));
+  return HG_OK;
+}
+
+static int weight_csr(HgOp* wop, const DevCsr** A, const double** vals) {
+  if (wop->kind == 0) {
+    *A = &wop->csr;
+    *vals = wop->csr.data;
+  } else if (wop->mode == 2 || wop->mode == 3) {
+    *A = &wop->P->A;
+    *vals = wop->mode == 2 ? wop->P->A.data : wop->P->A.data2;
+  } else {
+    set_error("weight must be a matrix operator (CSR, B or D_k)");
+    return HG_ERR_ARG;
+  }
+  if (!*vals) {
+    set_error("weight operator has no values");
+    return HG_ERR_ARG;
+  }
+  return HG_OK;
+}
+
+static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr, double* x, long long ldx, int nrhs,
+                       double rtol, int maxit, double* history, int32_t* info, cudaStream_t st) {
+  const int n = op->n;
+  const bool weighted = weight != nullptr;
+  const DevCsr* WA = nullptr;
+  const double* wvals = nullptr;
+  if (weighted) HG_TRY(weight_csr(weight, &WA, &wvals));
+  DcWs& ws = nrhs == 1 ? op->dws : op->dwsb;
+  HG_TRY(dws_reserve(ws, n, nrhs, maxit + 1, weighted));
+  const long long W2 = 2LL * (ws.cap + 2), Y2 = ws.cap + 2;
+  const long long vstride = (long long)nrhs * n;
+  const size_t vbytes = sizeof(double) * (size_t)n;
+  HG_TRY(ws.Q.ensure(vbytes * nrhs));
+  double* Q = ws.Q.ptr();
+  auto qv = [&](int i) { return Q + (long long)i * vstride; };
+  double* hdots = ws.hbuf;
+  double* hnrm = hdots + W2 * nrhs;
+  double* hcoef = hnrm + nrhs;
+  double* hy = hcoef + W2 * nrhs;
+  const int stride_h = maxit + 1;
+  for (int c = 0; c < nrhs; ++c) info[4 * c] = info[4 * c + 1] = info[4 * c + 2] = info[4 * c + 3] = 0;
+  ColList all{};
+  all.n = nrhs;
+  for (int c = 0; c < nrhs; ++c) all.c[c] = c;
+  int nb = 0, nbs = 0;
+
+  // q_0 = r0 / ||r0||_W (wgmres.py:102-115)
+  HG_CUDA_TRY(cudaMemcpy2DAsync(Q, vbytes, rhs, sizeof(double) * ldr, vbytes, nrhs, cudaMemcpyDeviceToDevice, st));
+  if (weighted) {
+    HG_TRY(launch_spmm_cols(*WA, wvals, Q, n, ws.wq, n, all, ws.pself, 1, &nbs, st));
+    HG_TRY(launch_reduce_batch(ws.pself, nbs, 1, 1, all, ws.nrm2, 1, st));
+  } else {
+    HG_TRY(launch_dots_batch(n, Q, n, nullptr, 0, 0, 0, all, ws.partials, 1, &nb, st));
+    HG_TRY(launch_reduce_batch(ws.partials, nb, 1, 1, all, ws.nrm2, 1, st));
+  }
+  HG_CUDA_TRY(cudaMemcpyAsync(hnrm, ws.nrm2, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, st));
+  HG_CUDA_TRY(cudaStreamSynchronize(st));
+
+  struct ColState {
+    double beta = 0.0;
+    std::vector<std::vector<double>> Hraw, Hrot;  // unrotated / rotated Hessenberg columns
+    std::vector<double> cs, sn, g;
+    int hist_len = 1;
+    bool converged = false, breakdown = false;
+  };
+  std::vector<ColState> cst(nrhs);
+  ColList act{}, zero{};
+  for (int c = 0; c < nrhs; ++c) {
+    ColState& S = cst[c];
+    S.beta = std::sqrt(hnrm[c]);
+    history[(long long)c * stride_h] = S.beta;
+    if (S.beta == 0.0 || maxit == 0) {
+      S.converged = S.beta == 0.0;
+      zero.c[zero.n++] = c;
+    } else {
+      S.g.assign(1, S.beta);
+      act.c[act.n++] = c;
+    }
+  }
+  HG_TRY(launch_fill_batch(n, x, ldx, zero, st));
+  HG_TRY(launch_fill_batch(n, Q, n, zero, st));
+  HG_TRY(launch_scale_dev_batch(n, Q, ws.wq, n, Q, n, weighted ? ws.wq : nullptr, ws.nrm2, act, st));
+  const double BREAKDOWN_RTOL = 1e-14;
+
+  // Givens rotation of the final column k (wgmres.py:158-184); true = stop
+  auto finalize = [&](int c, int k) -> bool {
+    ColState& S = cst[c];
+    std::vector<double> col = S.Hraw[k];
+    for (int i = 0; i < k; ++i) {
+      const double t = S.cs[i] * col[i] - S.sn[i] * col[i + 1];
+      col[i + 1] = S.sn[i] * col[i] + S.cs[i] * col[i + 1];
+      col[i] = t;
+    }
+    const double denom = std::hypot(col[k], col[k + 1]);
+    double csk = 1.0, snk = 0.0;
+    if (denom != 0.0) {
+      csk = col[k] / denom;
+      snk = -col[k + 1] / denom;
+    }
+    S.cs.push_back(csk);
+    S.sn.push_back(snk);
+    col[k] = csk * col[k] - snk * col[k + 1];
+    col[k + 1] = 0.0;
+    S.Hrot.push_back(col);
+    const double gk = S.g[k];
+    S.g.push_back(snk * gk);
+    S.g[k] = csk * gk;
+    const double res = std::fabs(S.g[k + 1]);
+    history[(long long)c * stride_h + S.hist_len++] = res;
+    if (res <= rtol * S.beta || S.breakdown) {
+      S.converged = true;
+      return true;
+    }
+    return false;
+  };
+
+  for (int j = 0; act.n > 0; ++j) {
+    const int nv = j + 1;
+    {
+      Phase ph(st, 0);
+      if (nrhs == 1)
+        HG_TRY(op_apply_dots(op, qv(j), ws.w, nullptr, 0, 0, nullptr, nullptr, st));
+      else
+        HG_TRY(op_apply_multi(op, qv(j), n, ws.w, n, nrhs, st));
+    }
+    const double* U = ws.w;
+    if (weighted) {
+      Phase ph(st, 6);
+      HG_TRY(launch_spmm_cols(*WA, wvals, ws.w, n, ws.u, n, act, nullptr, 0, nullptr, st));
+      U = ws.u;
+    }
+    {
+      Phase ph(st, 1);
+      HG_TRY(launch_dots2_batch(n, weighted ? ws.wq : qv(j), n, U, n, Q, vstride, n, nv, act, ws.partials, ws.dots,
+                                W2, st));
+    }
+    HG_CUDA_TRY(cudaMemcpy2DAsync(hdots, sizeof(double) * W2, ws.dots, sizeof(double) * W2, sizeof(double) * 2 * nv,
+                                  nrhs, cudaMemcpyDeviceToHost, st));
+    HG_CUDA_TRY(cudaMemcpyAsync(hnrm, ws.nrm2, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, st));
+    HG_CUDA_TRY(cudaStreamSynchronize(st));
+
+    ColList keep{}, done{};
+    for (int k = 0; k < act.n; ++k) {
+      const int c = act.c[k];
+      ColState& S = cst[c];
+      const double* a = hdots + c * W2;  // Q_i . W q_j
+      const double* z = a + nv;          // Q_i . W w
+      double rho = 1.0;
+      std::vector<double> s(j, 0.0);
+      bool stop = false;
+      if (j > 0) {
+        std::vector<double>& col = S.Hraw[j - 1];
+        const double beta = std::sqrt(std::max(hnrm[c], 0.0));
+        double cscale = beta;
+        for (int i = 0; i < j; ++i) cscale = std::max(cscale, std::fabs(col[i]));
+        if (beta <= BREAKDOWN_RTOL * std::max(cscale, 1e-300)) {  // lucky breakdown (wgmres.py:151-156)
+          col[j] = beta;
+          S.breakdown = true;
+          stop = finalize(c, j - 1);
+        } else {
+          double ss = 0.0;
+          for (int i = 0; i < j; ++i) {
+            s[i] = a[i];
+            ss += s[i] * s[i];
+          }
+          const double rho2 = a[j] - ss;
+          rho = rho2 > 0.0 ? std::sqrt(rho2) : std::sqrt(std::max(a[j], 1e-300));
+          for (int i = 0; i < j; ++i) col[i] += beta * s[i];
+          col[j] = beta * rho;
+          cscale = 0.0;
+          for (int i = 0; i <= j; ++i) cscale = std::max(cscale, std::fabs(col[i]));
+          if (col[j] <= BREAKDOWN_RTOL * std::max(cscale, 1e-300)) S.breakdown = true;
+          stop = finalize(c, j - 1);
+        }
+      }
+      if (!stop && j == maxit) stop = true;  // maxit columns finalised, not converged
+      if (stop) {
+        done.c[done.n++] = c;
+        continue;
+      }
+      // projection of A q_j (q_j corrected) onto Q_{0:j}
+      std::vector<double> col(j + 2, 0.0);
+      double* cf = hcoef + c * W2;
+      cf[0] = 1.0 / rho;
+      double sz = 0.0;
+      for (int i = 0; i < j; ++i) {
+        cf[1 + i] = s[i];
+        sz += s[i] * z[i];
+      }
+      for (int i = 0; i <= j; ++i) {
+        double hs = 0.0;  // (H s)_i over the corrected columns 0..j-1
+        for (int kk = std::max(0, i - 1); kk < j; ++kk) hs += S.Hraw[kk][i] * s[kk];
+        const double zp = (i < j) ? z[i] : (z[j] - sz) / rho;
+        const double h = (zp - hs) / rho;
+        col[i] = h;
+        cf[1 + j + i] = hs / rho + h;
+      }
+      S.Hraw.push_back(col);
+      keep.c[keep.n++] = c;
+    }
+    if (keep.n > 0 || done.n > 0) HG_TRY(ws.Q.ensure(vbytes * nrhs * std::min(j + 2, ws.cap)));
+    if (keep.n > 0) {
+      HG_CUDA_TRY(cudaMemcpy2DAsync(ws.coef, sizeof(double) * W2, hcoef, sizeof(double) * W2,
+                                    sizeof(double) * (2 * j + 2), nrhs, cudaMemcpyHostToDevice, st));
+      {
+        Phase ph(st, 2);
+        HG_TRY(launch_dcgs2_update(n, Q, vstride, n, j, ws.w, n, ws.coef, W2, keep, st));
+      }
+      {
+        Phase ph(st, 3);
+        if (weighted) {
+          HG_TRY(launch_spmm_cols(*WA, wvals, ws.w, n, ws.ww, n, keep, ws.pself, 1, &nbs, st));
+          HG_TRY(launch_reduce_batch(ws.pself, nbs, 1, 1, keep, ws.nrm2, 1, st));
+        } else {
+          HG_TRY(launch_dots_batch(n, ws.w, n, nullptr, 0, 0, 0, keep, ws.partials, 1, &nb, st));
+          HG_TRY(launch_reduce_batch(ws.partials, nb, 1, 1, keep, ws.nrm2, 1, st));
+        }
+      }
+      {
+        Phase ph(st, 5);
+        HG_TRY(launch_scale_dev_batch(n, ws.w, ws.ww, n, qv(j + 1), n, weighted ? ws.wq : nullptr, ws.nrm2, keep,
+                                      st));
+      }
+    }
+    if (done.n > 0 && j + 1 < ws.cap) HG_TRY(launch_fill_batch(n, qv(j + 1), n, done, st));
+    act = keep;
+  }
+  // x_c = Q_c y_c with y_c = R_c^{-1} g_c (wgmres.py:186-192)
+  std::vector<int> mlist(nrhs, 0);
+  for (int c = 0; c < nrhs; ++c) {
+    ColState& S = cst[c];
+    const int m = S.hist_len - 1;
+    mlist[c] = m;
+    double* y = hy + c * Y2;
+    for (int i = m - 1; i >= 0; --i) {
+      double sacc = S.g[i];
+      for (int k = i + 1; k < m; ++k) sacc -= S.Hrot[k][i] * y[k];
+      y[i] = sacc / S.Hrot[i][i];
+    }
+  }
+  HG_CUDA_TRY(cudaMemcpyAsync(ws.dy, hy, sizeof(double) * Y2 * nrhs, cudaMemcpyHostToDevice, st));
+  for (int c = 0; c < nrhs; ++c) {
+    ColList one{};
+    one.n = 1;
+    one.c[0] = c;
+    if (mlist[c] > 0)
+      HG_TRY(launch_axpy_batch(n, x, ldx, Q, vstride, n, mlist[c], ws.dy, Y2, 0, one, st));
+    else if (cst[c].beta != 0.0)
+      HG_TRY(launch_fill_batch(n, x, ldx, one, st));
+  }
+  HG_CUDA_TRY(cudaStreamSynchronize(st));
+  stats_collect();
+  for (int c = 0; c < nrhs; ++c) {
+    info[4 * c] = mlist[c];
+    info[4 * c + 1] = cst[c].converged ? 1 : 0;
+    info[4 * c + 2] = cst[c].breakdown ? 1 : 0;
+    info[4 * c + 3] = mlist[c] > 0 ? mlist[c] - 1 : 0;  // every column is reorthogonalised once
+  }
+  return HG_OK;
+}
+
+extern "C" int hg_set_orthogonalization(int mode) {
+  if (mode != HG_ORTH_MEASURED && mode != HG_ORTH_DCGS2) {
+    set_error("hg_set_orthogonalization: unknown mode");
+    return HG_ERR_ARG;
+  }
+  g_orth = mode;
+  return HG_OK;
+}
+
+extern "C" int hg_get_orthogonalization(void) { return g_orth; }
+
+// ------------------------------------------------------------------ batched GMRES
+// WW[:, c] = W X[:, c] for the listed columns, self dots X_c . WW_c into pself[c][nb]
+static int weight_apply_batch(HgOp* wop, const double* X, long long ldx, double* Y, long long ldy,
+                              const ColList& cols, double* pself, int* nb, cudaStream_t st) {
+  const DevCsr* A;
+  const double* vals;
+  if (wop->kind == 0) {
+    A = &wop->csr;
+    vals = wop->csr.data;
+  } else if (wop->mode == 2 || wop->mode == 3) {
+    A = &wop->P->A;
+    vals = wop->mode == 2 ? wop->P->A.data : wop->P->A.data2;
+  } else {
+    set_error("weight must be a matrix operator (CSR, B or D_k)");
+    return HG_ERR_ARG;
+  }
+  if (!vals) {
+    set_error("weight operator has no values");
+    return HG_ERR_ARG;
+  }
+  return launch_spmm_cols(*A, vals, X, ldx, Y, ldy, cols, pself, 1, nb, st);
+}
+
+static int bws_reserve(BatchWs& ws, int n, int nrhs, int cap, bool weighted) {
+  if (ws.n == n && ws.nrhs == nrhs && ws.cap >= cap && ws.weighted == weighted) return HG_OK;
+  ws.clear();
+  ws.n = n;
+  ws.nrhs = nrhs;
+  ws.cap = cap;
+  ws.weighted = weighted;
+  const size_t vbytes = sizeof(double) * (size_t)n * nrhs * cap;
+  HG_TRY(ws.V.reserve(vbytes));
+  if (weighted) HG_TRY(ws.WV.reserve(vbytes));
+  const size_t nn = (size_t)n * nrhs;
+  HG_CUDA_TRY(cudaMalloc(&ws.w, sizeof(double) * nn));
+  HG_CUDA_TRY(cudaMalloc(&ws.ww, sizeof(double) * nn));
+  const size_t nb = (size_t)ceil_div(n, VEC_TILE);
+  HG_CUDA_TRY(cudaMalloc(&ws.partials, sizeof(double) * nb * (cap + 2) * nrhs));
+  HG_CUDA_TRY(cudaMalloc(&ws.pself, sizeof(double) * (size_t)ceil_div(n, 256) * nrhs));
+  HG_CUDA_TRY(cudaMalloc(&ws.dh, sizeof(double) * (size_t)(cap + 2) * nrhs));
+  HG_CUDA_TRY(cudaMalloc(&ws.dc, sizeof(double) * (size_t)(cap + 2) * nrhs));
+  HG_CUDA_TRY(cudaMalloc(&ws.dy, sizeof(double) * (size_t)(cap + 2) * nrhs));
+  HG_CUDA_TRY(cudaMallocHost(&ws.hbuf, sizeof(double) * 2 * (size_t)(cap + 2) * nrhs));
+  return HG_OK;
+}
+
+extern "C" int hg_gmres_batch(HgOp* op, HgOp* weight, const double* rhs, int64_t ldr, double* x, int64_t ldx,
+                              int32_t nrhs, double rtol, int32_t maxit, double* history, int32_t* info,
+                              void* stream) {
+  if (!op || !rhs || !x || !history || !info || nrhs < 1 || nrhs > HG_MAX_RHS || ldr < op->n || ldx < op->n) {
+    set_error("hg_gmres_batch: bad argument");
+    return HG_ERR_ARG;
+  }
+  if (weight && weight->n != op->n) {
+    set_error("hg_gmres_batch: weight dimension mismatch");
+    return HG_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = op->n;
+  maxit = std::max(0, std::min(maxit, n));
+  if (g_orth == HG_ORTH_DCGS2) return gmres_dcgs2(op, weight, rhs, ldr, x, ldx, nrhs, rtol, maxit, history, info, st);
+  const bool weighted = weight != nullptr;
+  BatchWs& ws = op->bws;
+  HG_TRY(bws_reserve(ws, n, nrhs, maxit + 1, weighted));
+  const long long W2 = ws.cap + 2;                 // row pitch of dh / dc / dy / hbuf
+  const long long vstride = (long long)nrhs * n;   // basis vector i -> i+1 of one column
+  const size_t vec_bytes = sizeof(double) * (size_t)n;
+  HG_TRY(ws.V.ensure(vec_bytes * nrhs));
+  if (weighted) HG_TRY(ws.WV.ensure(vec_bytes * nrhs));
+  double* V = ws.V.ptr();
+  double* WV = weighted ? ws.WV.ptr() : V;
+  auto vec = [&](double* B, int i) { return B + (long long)i * vstride; };  // column 0 of basis vector i
+  double* hb = ws.hbuf;
+  double* hb2 = ws.hbuf + W2 * nrhs;
+  const int stride_h = maxit + 1;
+  for (int c = 0; c < nrhs; ++c) info[4 * c] = info[4 * c + 1] = info[4 * c + 2] = info[4 * c + 3] = 0;
+
+  ColList all{};
+  all.n = nrhs;
+  for (int c = 0; c < nrhs; ++c) all.c[c] = c;
+  int nb = 0, nbs = 0;
+  // r0 = rhs (x0 = 0), beta_c = ||r0_c||_W
+  HG_CUDA_TRY(cudaMemcpy2DAsync(V, vec_bytes, rhs, sizeof(double) * ldr, vec_bytes, nrhs, cudaMemcpyDeviceToDevice, st));
+  if (weighted) {
+    HG_TRY(weight_apply_batch(weight, V, n, WV, n, all, ws.pself, &nbs, st));
+    HG_TRY(launch_reduce_batch(ws.pself, nbs, 1, 1, all, ws.dc, W2, st));
+  } else {
+    HG_TRY(launch_dots_batch(n, V, n, nullptr, 0, 0, 0, all, ws.partials, 1, &nb, st));
+    HG_TRY(launch_reduce_batch(ws.partials, nb, 1, 1, all, ws.dc, W2, st));
+  }
+  HG_CUDA_TRY(cudaMemcpy2DAsync(hb, sizeof(double), ws.dc, sizeof(double) * W2, sizeof(double), nrhs,
+                                cudaMemcpyDeviceToHost, st));
+  HG_CUDA_TRY(cudaStreamSynchronize(st));
+
+  struct ColState {
+    double beta = 0.0;
+    std::vector<std::vector<double>> H;  // Givens-rotated Hessenberg columns
+    std::vector<double> cs, sn, g;
+    int hist_len = 1;
+    bool converged = false, breakdown = false;
+    int reorth = 0;
+  };
+  std::vector<ColState> cst(nrhs);
+  ColList act{}, zero{};
+  for (int c = 0; c < nrhs; ++c) {
+    ColState& S = cst[c];
+    S.beta = std::sqrt(hb[c]);
+    history[(long long)c * stride_h] = S.beta;
+    if (S.beta == 0.0) {
+      S.converged = true;
+      zero.c[zero.n++] = c;
+    } else {
+      S.g.assign(1, S.beta);
+      act.s[act.n] = S.beta;
+      act.c[act.n++] = c;
+    }
+  }
+  HG_TRY(launch_fill_batch(n, x, ldx, zero, st));
+  HG_TRY(launch_fill_batch(n, V, n, zero, st));  // finite op inputs for finished columns
+  HG_TRY(launch_scale_batch(n, V, WV, n, V, weighted ? WV : nullptr, n, act, st));
+  const double REORTH_TOL = 1e-12, BREAKDOWN_RTOL = 1e-14;
+  std::vector<double> col(maxit + 2, 0.0);
+
+  for (int j = 0; j < maxit && act.n > 0; ++j) {
+    const int nv = j + 1;
+    HG_TRY(ws.V.ensure(vec_bytes * nrhs * (j + 2)));
+    if (weighted) HG_TRY(ws.WV.ensure(vec_bytes * nrhs * (j + 2)));
+    {  // w_c = op(V_c[j]) for the whole batch (finished columns carry zeros)
+      Phase ph(st, 0);
+      HG_TRY(op_apply_multi(op, vec(V, j), n, ws.w, n, nrhs, st));
+    }
+    {  // classical pass: h_c = (W V_c)^T w_c ; w_c -= V_c h_c
+      Phase ph(st, 1);
+      HG_TRY(launch_dots_batch(n, ws.w, n, WV, vstride, n, nv, act, ws.partials, nv + 1, &nb, st));
+      HG_TRY(launch_reduce_batch(ws.partials, nb, nv + 1, nv + 1, act, ws.dh, W2, st));
+    }
+    {
+      Phase ph(st, 2);
+      HG_TRY(launch_axpy_batch(n, ws.w, n, V, vstride, n, nv, ws.dh + 1, W2, 1, act, st));
+    }
+    {  // measurement corr_c = (W V_c)^T w_c, then ww_c = W w_c with w_c . ww_c (slot 0)
+      Phase ph(st, 3);
+      HG_TRY(launch_dots_batch(n, ws.w, n, WV, vstride, n, nv, act, ws.partials, nv + 1, &nb, st));
+      HG_TRY(launch_reduce_batch(ws.partials, nb, nv + 1, nv + 1, act, ws.dc, W2, st));
+      if (weighted) {
+        HG_TRY(weight_apply_batch(weight, ws.w, n, ws.ww, n, act, ws.pself, &nbs, st));
+        HG_TRY(launch_reduce_batch(ws.pself, nbs, 1, 1, act, ws.dc, W2, st));
+      }
+    }
+    HG_CUDA_TRY(cudaMemcpy2DAsync(hb, sizeof(double) * W2, ws.dh, sizeof(double) * W2, sizeof(double) * (nv + 1),
+                                  nrhs, cudaMemcpyDeviceToHost, st));
+    HG_CUDA_TRY(cudaMemcpy2DAsync(hb2, sizeof(double) * W2, ws.dc, sizeof(double) * W2, sizeof(double) * (nv + 1),
+                                  nrhs, cudaMemcpyDeviceToHost, st));
+    HG_CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<std::vector<double>> cols(nrhs);
+    std::vector<double> hnorm(nrhs, 0.0);
+    ColList ro{};
+    for (int k = 0; k < act.n; ++k) {
+      const int c = act.c[k];
+      const double* h = hb + c * W2 + 1;
+      const double* dcc = hb2 + c * W2;
+      std::vector<double>& cc = cols[c];
+      cc.assign(j + 2, 0.0);
+      for (int i = 0; i < nv; ++i) cc[i] = h[i];
+      hnorm[c] = std::sqrt(std::max(dcc[0], 0.0));
+      double cmax = 0.0;
+      for (int i = 0; i < nv; ++i) cmax = std::max(cmax, std::fabs(dcc[1 + i]));
+      if (cmax > REORTH_TOL * std::max(hnorm[c], 1e-300)) {  // wgmres.py:142-148
+        for (int i = 0; i < nv; ++i) cc[i] += dcc[1 + i];
+        ro.c[ro.n++] = c;
+        ++cst[c].reorth;
+      }
+    }
+    if (ro.n > 0) {
+      Phase ph(st, 4);
+      HG_TRY(launch_axpy_batch(n, ws.w, n, V, vstride, n, nv, ws.dc + 1, W2, 1, ro, st));
+      if (weighted) {
+        HG_TRY(weight_apply_batch(weight, ws.w, n, ws.ww, n, ro, ws.pself, &nbs, st));
+        HG_TRY(launch_reduce_batch(ws.pself, nbs, 1, 1, ro, ws.dc, W2, st));
+      } else {
+        HG_TRY(launch_dots_batch(n, ws.w, n, nullptr, 0, 0, 0, ro, ws.partials, 1, &nb, st));
+        HG_TRY(launch_reduce_batch(ws.partials, nb, 1, 1, ro, ws.dc, W2, st));
+      }
+      HG_CUDA_TRY(cudaMemcpy2DAsync(hb2, sizeof(double), ws.dc, sizeof(double) * W2, sizeof(double), nrhs,
+                                    cudaMemcpyDeviceToHost, st));
+      HG_CUDA_TRY(cudaStreamSynchronize(st));
+      for (int k = 0; k < ro.n; ++k) hnorm[ro.c[k]] = std::sqrt(std::max(hb2[ro.c[k]], 0.0));
+    }
+    ColList scl{}, done{}, keep{};
+    for (int k = 0; k < act.n; ++k) {
+      const int c = act.c[k];
+      ColState& S = cst[c];
+      std::vector<double>& cc = cols[c];
+      cc[j + 1] = hnorm[c];
+      double cscale = 0.0;
+      for (int i = 0; i <= j + 1; ++i) cscale = std::max(cscale, std::fabs(cc[i]));
+      if (hnorm[c] <= BREAKDOWN_RTOL * std::max(cscale, 1e-300)) {
+        S.breakdown = true;
+      } else {
+        scl.s[scl.n] = hnorm[c];
+        scl.c[scl.n++] = c;
+      }
+      // Givens update (wgmres.py:158-171)
+      for (int i = 0; i < j; ++i) {
+        const double t = S.cs[i] * cc[i] - S.sn[i] * cc[i + 1];
+        cc[i + 1] = S.sn[i] * cc[i] + S.cs[i] * cc[i + 1];
+        cc[i] = t;
+      }
+      const double denom = std::hypot(cc[j], cc[j + 1]);
+      double csj = 1.0, snj = 0.0;
+      if (denom != 0.0) {
+        csj = cc[j] / denom;
+        snj = -cc[j + 1] / denom;
+      }
+      S.cs.push_back(csj);
+      S.sn.push_back(snj);
+      cc[j] = csj * cc[j] - snj * cc[j + 1];
+      cc[j + 1] = 0.0;
+      S.H.push_back(cc);
+      const double gj = S.g[j];
+      S.g.push_back(snj * gj);
+      S.g[j] = csj * gj;
+      const double res = std::fabs(S.g[j + 1]);
+      history[(long long)c * stride_h + S.hist_len++] = res;
+      if (res <= rtol * S.beta || S.breakdown) {
+        S.converged = true;
+        done.c[done.n++] = c;
+      } else {
+        keep.s[keep.n] = act.s[k];
+        keep.c[keep.n++] = c;
+      }
+    }
+    {
+      Phase ph(st, 5);
+      HG_TRY(launch_scale_batch(n, ws.w, ws.ww, n, vec(V, j + 1), weighted ? vec(WV, j + 1) : nullptr, n, scl,
+                                st));
+      HG_TRY(launch_fill_batch(n, vec(V, j + 1), n, done, st));  // finished columns feed zeros to the op
+    }
+    act = keep;
+  }
+  // x_c = V_c y_c, y_c = H_c^{-1} g_c (host back substitution, wgmres.py:186-192)
+  std::vector<int> mlist(nrhs, 0);
+  for (int c = 0; c < nrhs; ++c) {
+    ColState& S = cst[c];
+    const int m = S.hist_len - 1;
+    mlist[c] = m;
+    double* y = hb + c * W2;
+    for (int i = m - 1; i >= 0; --i) {
+      double s = S.g[i];
+      for (int k = i + 1; k < m; ++k) s -= S.H[k][i] * y[k];
+      y[i] = s / S.H[i][i];
+    }
+  }
+  HG_CUDA_TRY(cudaMemcpyAsync(ws.dy, hb, sizeof(double) * W2 * nrhs, cudaMemcpyHostToDevice, st));
+  for (int c = 0; c < nrhs; ++c) {
+    ColList one{};
+    one.n = 1;
+    one.c[0] = c;
+    if (mlist[c] > 0)
+      HG_TRY(launch_axpy_batch(n, x, ldx, V, vstride, n, mlist[c], ws.dy, W2, 0, one, st));
+    else if (cst[c].beta != 0.0)
+      HG_TRY(launch_fill_batch(n, x, ldx, one, st));
+  }
+  HG_CUDA_TRY(cudaStreamSynchronize(st));
+  stats_collect();
+  for (int c = 0; c < nrhs; ++c) {
+    info[4 * c] = mlist[c];
+    info[4 * c + 1] = cst[c].converged ? 1 : 0;
+    info[4 * c + 2] = cst[c].breakdown ? 1 : 0;
+    info[4 * c + 3] = cst[c].reorth;
+  }
+  return HG_OK;
+}
+
+extern "C" int hg_solve_host_batch(HgPrecond* P, const double* F_host, double* X_host, int32_t nrhs, double rtol,
+                                   int32_t maxit, double* history, int32_t* info, void* stream) {
+  if (!P || !F_host || !X_host || nrhs < 1 || nrhs > HG_MAX_RHS) {
+    set_error("hg_solve_host_batch: bad argument");
+    return HG_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = P->n;
+  HG_TRY(ensure_solve_ops(P));
+  const size_t bytes = sizeof(double) * (size_t)n * nrhs;
+  double *d_f = nullptr, *d_rhs = nullptr, *d_x = nullptr;
+  HG_CUDA_TRY(cudaMallocAsync(&d_f, bytes, st));
+  HG_CUDA_TRY(cudaMallocAsync(&d_rhs, bytes, st));
+  HG_CUDA_TRY(cudaMallocAsync(&d_x, bytes, st));
+  HG_CUDA_TRY(cudaMemcpyAsync(d_f, F_host, bytes, cudaMemcpyHostToDevice, st));
+  int s = precond_apply_multi_core(P, d_f, n, d_rhs, n, nrhs, st);
+  if (s == HG_OK)
+    s = hg_gmres_batch(P->op_T, P->A.data2 ? P->op_W : nullptr, d_rhs, n, d_x, n, nrhs, rtol, maxit, history, info,
+                       stream);
+  if (s == HG_OK) HG_CUDA_TRY(cudaMemcpyAsync(X_host, d_x, bytes, cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(d_f, st);
+  cudaFreeAsync(d_rhs, st);
+  cudaFreeAsync(d_x, st);
+  HG_CUDA_TRY(cudaStreamSynchronize(st));
+  return s;
+}

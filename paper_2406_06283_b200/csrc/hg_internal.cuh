@@ -84,6 +84,17 @@ struct HgPrecond {
   long long* d_cent = nullptr;
 
   double* d_tmp = nullptr;        // n-vector scratch (B u for apply_T)
+
+  // multi-RHS scratch (allocated on the first batched call, HG_MAX_RHS columns)
+  bool multi_ready = false;
+  double* d_xsm = nullptr;        // [c][xs_len] local solutions
+  double* d_zsm = nullptr;        // [c][zs_len] Z_b Y_b rows
+  double* d_cpartm = nullptr;     // [part_len][HG_MAX_RHS] Z^T R partials
+  double* d_ym = nullptr;         // [m][HG_MAX_RHS] coarse solution
+  double* d_b0m_x = nullptr;      // [2][K*64][HG_MAX_RHS] phase solutions
+  unsigned long long* d_b0m_done = nullptr;  // monotone panel counter of the batched coarse solve
+  unsigned long long b0m_epoch = 0;
+  double* d_tmpm = nullptr;       // [c][n] scratch (B U for the batched apply_T)
   cudaStream_t aux = nullptr;     // coarse chain runs here, forked/joined per apply
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   long long device_bytes = 0;
@@ -141,6 +152,7 @@ int launch_spmv_dots(const DevCsr& A, const double* vals, const double* x, doubl
 int spmv_dots_nblocks(int n);
 
 int launch_local_solve(HgPrecond* P, const double* r, cudaStream_t st);
+int launch_local_solve_multi(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st);
 int launch_local_solve_single(HgPrecond* P, int s, const double* r_local, double* x_local, cudaStream_t st);
 int launch_zt(HgPrecond* P, const double* r, cudaStream_t st);
 // zt_target: value of the Z^T r chunk counter the solve waits for before reading c
@@ -149,6 +161,7 @@ int launch_coarse_solve_cluster(HgPrecond* P, cudaStream_t st, unsigned long lon
 size_t b0_cluster_smem(int NR);
 // force-load kernels at handle creation (see preload_local in hg_local.cu)
 int preload_local(HgPrecond* P);
+int preload_local_multi(HgPrecond* P);
 int preload_coarse();
 int preload_assemble();
 int preload_b0();
@@ -159,6 +172,59 @@ int launch_zy(HgPrecond* P, cudaStream_t st);
 int launch_assemble(HgPrecond* P, bool with_coarse, bool with_local, double* out, const double* W,
                     long long ldw, int nv, double* partials, int* nblocks_out, cudaStream_t st);
 int assemble_nblocks(int n);
+
+struct ColList {
+  int n;
+  int c[HG_MAX_RHS];
+  double s[HG_MAX_RHS];   // per-column scalar (h norms for scale)
+};
+
+// ---- multi-RHS (hg_multi.cu); batches are column c at base + c * ld
+int multi_prepare(HgPrecond* P);
+int preload_multi();
+int launch_spmm(const DevCsr& A, const double* vals, const double* X, long long ldx, double* Y, long long ldy,
+                int nrhs, cudaStream_t st);
+// Y = A X with per-column self dots X_c . Y_c into partials[(c * nb + b) * width]
+int launch_spmm_cols(const DevCsr& A, const double* vals, const double* X, long long ldx, double* Y, long long ldy,
+                     const ColList& cols, double* partials, int width, int* nb_out, cudaStream_t st);
+int launch_spmm_self(const DevCsr& A, const double* vals, const double* X, long long ldx, double* Y,
+                     long long ldy, int nrhs, double* partials, int width, int* nblocks_out, cudaStream_t st);
+int launch_zt_multi(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st);
+int launch_b0_multi(HgPrecond* P, int nrhs, cudaStream_t st, unsigned long long zt_target);
+int launch_zy_multi(HgPrecond* P, int nrhs, cudaStream_t st);
+int launch_assemble_multi(HgPrecond* P, bool with_coarse, bool with_local, double* OUT, long long ldo, int nrhs,
+                          cudaStream_t st);
+
+// Batched Arnoldi kernels over a list of columns (cols: device, ncols
+// entries).  Column c's vectors: z + c * ldz; its basis vector i:
+// V + c * ldcol + i * ldv.  Partials: [(c * nb + b) * width + slot].
+
+int launch_dots_batch(int n, const double* z, long long ldz, const double* V, long long ldv, long long ldcol,
+                      int nv, const ColList& cols, double* partials, int width, int* nblocks_out, cudaStream_t st);
+// out[c * ow + k] = sum_b partials[(c * nb + b) * width + k], k < cnt, for the listed columns
+int launch_reduce_batch(const double* partials, int nb, int width, int cnt, const ColList& cols, double* out,
+                        long long ow, cudaStream_t st);
+// mode 0: w = V coef ; 1: w -= V coef ; 2: w += V coef ; coef of column c at coef + c * ldcoef (+ coef_off)
+int launch_axpy_batch(int n, double* w, long long ldw, const double* V, long long ldv, long long ldcol, int nv,
+                      const double* coef, long long ldcoef, int mode, const ColList& cols, cudaStream_t st);
+// V_c = w_c / s_c, WV_c = ww_c / s_c for the listed columns
+int launch_scale_batch(int n, const double* w, const double* ww, long long ldw, double* V, double* WV,
+                       long long ldcol, const ColList& cols, cudaStream_t st);
+int launch_fill_batch(int n, double* y, long long ldy, const ColList& cols, cudaStream_t st);
+// DCGS2 Arnoldi (hg_multi.cu): dots of V_c[0..nv) with A_c and U_c in one basis read
+// (partials [(c * nb + b) * width + {i, nv + i}]); the fused delayed
+// reorthogonalisation / projection update; device-normalised append.
+// (reduced into out[c * ow + k], k < 2 nv: V_k . A_c then V_k . U_c)
+int launch_dots2_batch(int n, const double* A, long long lda, const double* U, long long ldu, const double* V,
+                       long long ldv, long long ldcol, int nv, const ColList& cols, double* partials, double* out,
+                       long long ow, cudaStream_t st);
+int launch_dcgs2_update(int n, double* V, long long ldv, long long ldcol, int j, double* w, long long ldw,
+                        const double* coef, long long ldcoef, const ColList& cols, cudaStream_t st);
+int launch_scale_dev_batch(int n, const double* w, const double* ww, long long ldw, double* V, long long ldcol,
+                           double* Wq, const double* nrm2, const ColList& cols, cudaStream_t st);
+int preload_dcgs2();
+int preload_add();
+int launch_add(int n, const double* a, const double* b, double* out, cudaStream_t st);  // out = a + b
 
 // Arnoldi helpers
 int launch_dots(int n, const double* z, const double* W, long long ldw, int nv, double* partials,

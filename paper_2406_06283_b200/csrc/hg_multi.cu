@@ -1,0 +1,887 @@
+// Multi-RHS (batched) solve phase — SURVEY §8a row a15: BASELINE config 5's
+// 16 seeded right-hand sides solved as one batch.  There is no reference
+// function; the oracle is the one-at-a-time path (schwarz.py:51-61 per
+// column).  Every kernel here keeps the columns independent (column c of an
+// output depends only on column c of the input), so a batch is exactly nrhs
+// single solves sharing the operator streams:
+//
+//  k_spmm        Y = A X for up to 16 columns, the CSR row read once; each
+//                column summed in index order without FMA (bitwise equal to
+//                scipy's csr_matvec, like k_spmv); optional self dots X.Y.
+//  k_zt_multi    C_b = Z_b^T R_b per (block, 256-row chunk) as a dense FP64
+//                contraction on the tensor pipe (DMMA m8n8k4): A = Z^T read
+//                once from HBM, B = the gathered 256 x 16 R chunk in smem.
+//  k_b0_multi    Y = B0^{-1} C with the tiled getrf factors (hg_b0.cu /
+//                hg_b0c.cu layout): persistent CTAs, panel t owned by CTA
+//                t % G, each 64 x 64 x 16 tile product on DMMA, panels
+//                published through a monotone L2 counter (release/acquire).
+//  k_zy_multi    U_b = Z_b Y_b (256 rows x m_b x 16) on DMMA.
+//  k_assemble_multi  out = coarse + local contributions in the reference's
+//                fixed summation order (schwarz.py:52-61), per column.
+//  batched Arnoldi helpers (dots / reduce / axpy / scale over a column list).
+#include <algorithm>
+#include <cstdlib>
+
+#include "hg_internal.cuh"
+
+namespace hg {
+
+constexpr int MR = HG_MAX_RHS;  // layout stride of the [row][rhs] coarse batch arrays
+constexpr int SR = 20;          // smem row stride (doubles) of 16-column operand tiles:
+                                // conflict-free DMMA B-fragment loads (20 = 4 mod 16)
+constexpr int ZROWS = 256;      // rows per Z^T R / Z Y work item (the k_zt chunking)
+
+// D = A B + D, m8n8k4 FP64 (DMMA).  Fragments (lane = 4 g + q):
+//   A[g][q], B[q][g], D[g][2q], D[g][2q+1].
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+// ------------------------------------------------------------------ SpMM
+__global__ void __launch_bounds__(256) k_spmm(int n, const int* __restrict__ ip, const int* __restrict__ ix,
+                                              const double* __restrict__ a, const double* __restrict__ X,
+                                              long long ldx, double* __restrict__ Y, long long ldy, ColList cols,
+                                              double* __restrict__ partials, int width, int nb) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  const int nr = cols.n;
+  double s[MR];
+#pragma unroll
+  for (int c = 0; c < MR; ++c) s[c] = 0.0;
+  if (i < n) {
+    const int e1 = ip[i + 1];
+    for (int e = ip[i]; e < e1; ++e) {
+      const double av = a[e];
+      const int col = ix[e];
+#pragma unroll
+      for (int c = 0; c < MR; ++c)
+        if (c < nr) s[c] = __dadd_rn(s[c], __dmul_rn(av, __ldg(X + (long long)cols.c[c] * ldx + col)));
+    }
+#pragma unroll
+    for (int c = 0; c < MR; ++c)
+      if (c < nr) Y[(long long)cols.c[c] * ldy + i] = s[c];
+  }
+  if (partials) {  // self dots X_c . Y_c, fixed-order block reduction per column
+    __shared__ double s_w[8][MR];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int c = 0; c < MR; ++c) {
+      if (c < nr) {
+        double v = i < n ? __ldg(X + (long long)cols.c[c] * ldx + i) * s[c] : 0.0;
+        v = warp_sum(v);
+        if (lane == 0) s_w[warp][c] = v;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < nr) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += s_w[w][threadIdx.x];
+      partials[((long long)cols.c[threadIdx.x] * nb + blockIdx.x) * width] = t;
+    }
+  }
+}
+
+static ColList all_cols(int nrhs) {
+  ColList c{};
+  c.n = nrhs;
+  for (int k = 0; k < nrhs; ++k) c.c[k] = k;
+  return c;
+}
+
+static int spmm_impl(const DevCsr& A, const double* vals, const double* X, long long ldx, double* Y, long long ldy,
+                     const ColList& cols, double* partials, int width, int* nb_out, cudaStream_t st) {
+  const int nb = ceil_div(A.n, 256);
+  if (nb_out) *nb_out = nb;
+  if (A.n == 0 || cols.n == 0) return HG_OK;
+  if (cols.n > MR) {
+    set_error("spmm: more than HG_MAX_RHS columns");
+    return HG_ERR_ARG;
+  }
+  k_spmm<<<nb, 256, 0, st>>>(A.n, A.indptr, A.indices, vals, X, ldx, Y, ldy, cols, partials, width, nb);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+int launch_spmm(const DevCsr& A, const double* vals, const double* X, long long ldx, double* Y, long long ldy,
+                int nrhs, cudaStream_t st) {
+  return spmm_impl(A, vals, X, ldx, Y, ldy, all_cols(nrhs), nullptr, 0, nullptr, st);
+}
+
+int launch_spmm_cols(const DevCsr& A, const double* vals, const double* X, long long ldx, double* Y, long long ldy,
+                     const ColList& cols, double* partials, int width, int* nb_out, cudaStream_t st) {
+  return spmm_impl(A, vals, X, ldx, Y, ldy, cols, partials, width, nb_out, st);
+}
+
+int launch_spmm_self(const DevCsr& A, const double* vals, const double* X, long long ldx, double* Y, long long ldy,
+                     int nrhs, double* partials, int width, int* nb_out, cudaStream_t st) {
+  return spmm_impl(A, vals, X, ldx, Y, ldy, all_cols(nrhs), partials, width, nb_out, st);
+}
+
+// ------------------------------------------------------------------ Z^T R
+__global__ void __launch_bounds__(256) k_zt_multi(const int2* __restrict__ items, const CblkDesc* __restrict__ descs,
+                                                  const int* __restrict__ idx, const double* __restrict__ Z,
+                                                  const double* __restrict__ R, long long ldr, int nrhs,
+                                                  double* __restrict__ cpartm, unsigned long long* __restrict__ done) {
+  __shared__ __align__(16) double s_r[ZROWS * SR];
+  const int2 it = items[blockIdx.x];
+  const CblkDesc d = descs[it.x];
+  const int k0 = it.y * ZROWS, rows = min(ZROWS, d.n - k0);
+  const int* ib = idx + d.idx_off + k0;
+  for (int e = threadIdx.x; e < ZROWS * MR; e += 256) {  // gather the chunk, zero padded
+    const int k = e % ZROWS, c = e / ZROWS;
+    double v = 0.0;
+    if (k < rows && c < nrhs) v = __ldg(R + (long long)c * ldr + __ldg(ib + k));
+    s_r[k * SR + c] = v;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, g = lane >> 2;
+  const double* zb = Z + d.z_off + (long long)k0 * d.m;
+  for (int i0 = warp * 8; i0 < d.m; i0 += 64) {  // 8 coarse columns of the block per warp
+    const int col = i0 + g;
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+#pragma unroll 8
+    for (int ks = 0; ks < ZROWS; ks += 4) {
+      const int k = ks + q;
+      const double a = (k < rows && col < d.m) ? __ldg(zb + (long long)k * d.m + col) : 0.0;  // A = Z^T
+      dmma(c0, a, s_r[k * SR + g]);
+      dmma(c1, a, s_r[k * SR + 8 + g]);
+    }
+    if (col < d.m) {
+      double* dst = cpartm + (d.part_off + (long long)it.y * d.m + col) * MR;
+      *reinterpret_cast<double2*>(dst + 2 * q) = make_double2(c0[0], c0[1]);
+      *reinterpret_cast<double2*>(dst + 8 + 2 * q) = make_double2(c1[0], c1[1]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // chunk complete: the batched coarse solve may be waiting for it
+    __threadfence();
+    atomicAdd(done, 1ull);
+  }
+}
+
+int launch_zt_multi(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st) {
+  if (P->m == 0 || P->n_zt_items == 0) return HG_OK;
+  k_zt_multi<<<P->n_zt_items, 256, 0, st>>>(P->d_zt_items, P->d_cblk, P->d_cblk_idx, P->d_z, R, ldr, nrhs,
+                                             P->d_cpartm, P->d_zt_done);
+  HG_LAUNCH_CHECK();
+  P->zt_epoch += (unsigned long long)P->n_zt_items;
+  return HG_OK;
+}
+
+// ------------------------------------------------------------------ Z Y
+__global__ void __launch_bounds__(256) k_zy_multi(const int2* __restrict__ items, const CblkDesc* __restrict__ descs,
+                                                  const double* __restrict__ Z, const double* __restrict__ ym,
+                                                  int nrhs, double* __restrict__ zsm, long long zs_len) {
+  __shared__ __align__(16) double s_y[64 * SR];
+  const int2 it = items[blockIdx.x];
+  const CblkDesc d = descs[it.x];
+  const int k0 = it.y * ZROWS, rows = min(ZROWS, d.n - k0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, g = lane >> 2;
+  double acc[4][2][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) acc[t][h][0] = acc[t][h][1] = 0.0;
+  const double* zb = Z + d.z_off + (long long)k0 * d.m;
+  for (int l0 = 0; l0 < d.m; l0 += 64) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 64 * MR; e += 256) {
+      const int l = e / MR, c = e % MR;
+      s_y[l * SR + c] = (l0 + l < d.m && c < nrhs) ? ym[(long long)(d.col0 + l0 + l) * MR + c] : 0.0;
+    }
+    __syncthreads();
+    const int lc = min(64, d.m - l0);
+    for (int ks = 0; ks < lc; ks += 4) {
+      const int l = ks + q;
+      const double b0 = s_y[l * SR + g], b1 = s_y[l * SR + 8 + g];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int row = warp * 32 + t * 8 + g;
+        const double a = (row < rows && l0 + l < d.m) ? __ldg(zb + (long long)row * d.m + l0 + l) : 0.0;
+        dmma(acc[t][0], a, b0);
+        dmma(acc[t][1], a, b1);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int row = warp * 32 + t * 8 + g;
+    if (row >= rows) continue;
+    double* dst = zsm + d.idx_off + k0 + row;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * h + 2 * q + e;
+        if (c < nrhs) dst[(long long)c * zs_len] = acc[t][h][e];
+      }
+  }
+}
+
+int launch_zy_multi(HgPrecond* P, int nrhs, cudaStream_t st) {
+  if (P->m == 0 || P->n_zt_items == 0) return HG_OK;
+  k_zy_multi<<<P->n_zt_items, 256, 0, st>>>(P->d_zt_items, P->d_cblk, P->d_z, P->d_ym, nrhs, P->d_zsm, P->zs_len);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+// ------------------------------------------------------------------ B0^{-1}
+namespace {
+constexpr int BP = 64;
+constexpr int BTILE = BP * BP;
+
+__device__ __forceinline__ unsigned long long ld_acq(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_rel(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// element (r, c) of a 64 x 64 tile; swizzled tiles (cluster layout,
+// factor.swizzle_tile_rows) keep 16-byte chunk c/2 of row r at chunk
+// (c/2) ^ ((r & 1) << 2)
+__device__ __forceinline__ int tidx(int r, int c, int swz) {
+  return r * BP + (swz ? ((((c >> 1) ^ ((r & 1) << 2)) << 1) | (c & 1)) : c);
+}
+
+// this lane's 16 A fragments of rows `row` of a tile (scaled by sign)
+__device__ __forceinline__ void load_afrag(double (&av)[16], const double* __restrict__ T, int row, int q, int swz,
+                                           double sign) {
+#pragma unroll
+  for (int s = 0; s < 16; ++s) av[s] = sign * __ldg(T + tidx(row, 4 * s + q, swz));
+}
+
+// acc (8 x 16 rows of this warp) += A (this warp's 8 tile rows) * X (64 x 16, smem)
+__device__ __forceinline__ void mma_tile(double (&acc)[2][2], const double (&av)[16], const double* s_x, int q, int g) {
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    const int k = 4 * s + q;
+    dmma(acc[0], av[s], s_x[k * SR + g]);
+    dmma(acc[1], av[s], s_x[k * SR + 8 + g]);
+  }
+}
+}  // namespace
+
+struct B0MultiArgs {
+  int m, K, nrhs, premul, swz;
+  const int* perm;
+  const int* col_blk;
+  const CblkDesc* descs;
+  const double* cpartm;     // [part][MR]
+  const double* dinv;       // [2K][64][64]
+  const long long* tile_ptr;
+  const int* tile_col;
+  const double* tiles;      // [ntile][64][64]
+  double* xbuf;             // [2][K*64][MR]
+  double* y;                // [m][MR]
+  unsigned long long* done;
+  unsigned long long base;
+  const unsigned long long* zt_done;
+  unsigned long long zt_target;
+};
+
+// Panel g (phase ph = g / K: 0 = L solve of P c, 1 = U solve in reversed
+// coordinates of the L solution) of 64 rows x nrhs columns; warp w owns
+// panel rows 8w..8w+7.  premul (cluster layout): tiles are D_t^{-1} T[t, j]
+// and x_t = D_t^{-1} rhs_t - sum_j M[t, j] x_j; otherwise
+// x_t = D_t^{-1} (rhs_t - sum_j T[t, j] x_j).  Tiles in ascending j: the
+// summation order is fixed, the result deterministic.
+__global__ void __launch_bounds__(256, 1) k_b0_multi(B0MultiArgs a) {
+  __shared__ __align__(16) double s_x[BP * SR];
+  __shared__ unsigned long long s_seen;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = lane & 3, g8 = lane >> 2;
+  const int row = warp * 8 + g8;
+  const int K = a.K;
+  auto observe = [&](unsigned long long need) -> unsigned long long {
+    if (tid == 0) {
+      unsigned long long v = ld_acq(a.done);
+      while (v < need) v = ld_acq(a.done);
+      s_seen = v;
+    }
+    __syncthreads();
+    return s_seen;
+  };
+  if (tid == 0)
+    while (ld_acq(a.zt_done) < a.zt_target) {
+    }
+  __syncthreads();
+  unsigned long long seen = 0;
+  for (int g = blockIdx.x; g < 2 * K; g += gridDim.x) {
+    const int ph = g / K, t = g % K;
+    const unsigned long long pbase = a.base + (unsigned long long)ph * K;
+    const double* dinv_g = a.dinv + (size_t)g * BTILE;
+    double av[16];
+    if (a.premul) load_afrag(av, dinv_g, row, q, a.swz, 1.0);
+    if (ph == 1 && seen < a.base + K) seen = observe(a.base + K);  // the whole L solve
+    __syncthreads();  // s_x free
+    for (int e = tid; e < BP * MR; e += 256) {
+      const int r = e / MR, c = e % MR;
+      double v = 0.0;
+      if (c < a.nrhs) {
+        if (ph == 0) {
+          const int i = t * BP + r;
+          if (i < a.m) {
+            const int col = a.perm[i];
+            const CblkDesc d = a.descs[a.col_blk[col]];
+            const int l = col - d.col0;
+            for (int ch = 0; ch < d.nchunk; ++ch) v += a.cpartm[(d.part_off + (long long)ch * d.m + l) * MR + c];
+          }
+        } else {
+          v = a.xbuf[((size_t)K * BP - 1 - (t * BP + r)) * MR + c];
+        }
+      }
+      s_x[r * SR + c] = v;
+    }
+    __syncthreads();
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    if (a.premul) {
+      mma_tile(acc, av, s_x, q, g8);
+    } else {
+      acc[0][0] = s_x[row * SR + 2 * q];
+      acc[0][1] = s_x[row * SR + 2 * q + 1];
+      acc[1][0] = s_x[row * SR + 8 + 2 * q];
+      acc[1][1] = s_x[row * SR + 8 + 2 * q + 1];
+    }
+    const long long e0 = a.tile_ptr[g], e1 = a.tile_ptr[g + 1];
+    for (long long e = e0; e < e1; ++e) {
+      const int j = a.tile_col[e];
+      load_afrag(av, a.tiles + (size_t)e * BTILE, row, q, a.swz, -1.0);  // in flight across the wait
+      if (seen < pbase + j + 1) seen = observe(pbase + j + 1);
+      __syncthreads();  // s_x free
+      {
+        const double2* src = reinterpret_cast<const double2*>(a.xbuf + ((size_t)(ph * K + j) * BP) * MR);
+        for (int e2 = tid; e2 < BP * MR / 2; e2 += 256) {
+          const double2 v = src[e2];
+          const int r = (2 * e2) / MR, c = (2 * e2) % MR;
+          *reinterpret_cast<double2*>(s_x + r * SR + c) = v;
+        }
+      }
+      __syncthreads();
+      mma_tile(acc, av, s_x, q, g8);
+    }
+    if (!a.premul) {  // x_t = D_t^{-1} acc
+      load_afrag(av, dinv_g, row, q, a.swz, 1.0);
+      __syncthreads();
+      *reinterpret_cast<double2*>(s_x + row * SR + 2 * q) = make_double2(acc[0][0], acc[0][1]);
+      *reinterpret_cast<double2*>(s_x + row * SR + 8 + 2 * q) = make_double2(acc[1][0], acc[1][1]);
+      __syncthreads();
+      acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.0;
+      mma_tile(acc, av, s_x, q, g8);
+    }
+    double* xo = a.xbuf + ((size_t)(ph * K + t) * BP + row) * MR;
+    *reinterpret_cast<double2*>(xo + 2 * q) = make_double2(acc[0][0], acc[0][1]);
+    *reinterpret_cast<double2*>(xo + 8 + 2 * q) = make_double2(acc[1][0], acc[1][1]);
+    if (ph == 1) {
+      const int i = K * BP - 1 - (t * BP + row);
+      if (i < a.m) {
+        double* yo = a.y + (size_t)i * MR;
+        *reinterpret_cast<double2*>(yo + 2 * q) = make_double2(acc[0][0], acc[0][1]);
+        *reinterpret_cast<double2*>(yo + 8 + 2 * q) = make_double2(acc[1][0], acc[1][1]);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {  // publish in panel order (release covers the CTA's stores ordered by the barrier)
+      __threadfence();
+      while (ld_acq(a.done) < a.base + g) {
+      }
+      st_rel(a.done, a.base + g + 1);
+    }
+  }
+}
+
+int launch_b0_multi(HgPrecond* P, int nrhs, cudaStream_t st, unsigned long long zt_target) {
+  if (P->m == 0) return HG_OK;
+  if (P->b0_P != BP) {
+    set_error("batched coarse solve: needs 64-row panels (HG_B0_PANEL=64)");
+    return HG_ERR_UNSUPPORTED;
+  }
+  const int K = P->b0_K;
+  static const int env_g = getenv("HG_B0M_CTAS") ? atoi(getenv("HG_B0M_CTAS")) : 0;
+  const int G = std::min(K, env_g > 0 ? env_g : 16);
+  B0MultiArgs a{P->m, K, nrhs, P->b0_mode == 1 ? 1 : 0, P->b0_mode == 1 ? 1 : 0, P->d_b0_perm, P->d_col_blk,
+                P->d_cblk, P->d_cpartm, P->d_b0_dinv, P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles,
+                P->d_b0m_x, P->d_ym, P->d_b0m_done, P->b0m_epoch, P->d_zt_done, zt_target};
+  P->b0m_epoch += 2ull * K;
+  k_b0_multi<<<G, 256, 0, st>>>(a);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+// ------------------------------------------------------------------ assembly
+__global__ void __launch_bounds__(256) k_assemble_multi(int n, const int* __restrict__ cptr,
+                                                        const long long* __restrict__ cent,
+                                                        const double* __restrict__ zsm, long long zs_len,
+                                                        const int* __restrict__ lptr,
+                                                        const long long* __restrict__ lent,
+                                                        const double* __restrict__ xsm, long long xs_len,
+                                                        double* __restrict__ out, long long ldo) {
+  const int d = blockIdx.x * 256 + threadIdx.x;
+  const int c = blockIdx.y;
+  if (d >= n) return;
+  double acc = 0.0;
+  if (cptr) {
+    const double* z = zsm + (long long)c * zs_len;
+    for (int e = cptr[d]; e < cptr[d + 1]; ++e) acc += z[cent[e]];
+  }
+  if (lptr) {
+    const double* x = xsm + (long long)c * xs_len;
+    for (int e = lptr[d]; e < lptr[d + 1]; ++e) acc += x[lent[e]];
+  }
+  out[(long long)c * ldo + d] = acc;
+}
+
+int launch_assemble_multi(HgPrecond* P, bool with_coarse, bool with_local, double* OUT, long long ldo, int nrhs,
+                          cudaStream_t st) {
+  if (P->n == 0 || nrhs == 0) return HG_OK;
+  const bool coarse = with_coarse && P->m > 0;
+  k_assemble_multi<<<dim3(ceil_div(P->n, 256), nrhs), 256, 0, st>>>(
+      P->n, coarse ? P->d_cptr : nullptr, P->d_cent, P->d_zsm, P->zs_len, with_local ? P->d_lptr : nullptr,
+      P->d_lent, P->d_xsm, P->xs_len, OUT, ldo);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+// ------------------------------------------------------------------ batched Arnoldi
+__global__ void __launch_bounds__(VEC_THREADS) k_dots_batch(int n, const double* __restrict__ z, long long ldz,
+                                                            const double* __restrict__ V, long long ldv,
+                                                            long long ldcol, int nv, ColList cols,
+                                                            double* __restrict__ partials, int width, int nb) {
+  const int c = cols.c[blockIdx.y];
+  const double* zc = z + (long long)c * ldz;
+  double zv[VEC_ROWS];
+  int rows[VEC_ROWS];
+  double self = 0.0;
+#pragma unroll
+  for (int k = 0; k < VEC_ROWS; ++k) {
+    const int i = blockIdx.x * VEC_TILE + k * VEC_THREADS + threadIdx.x;
+    rows[k] = i;
+    zv[k] = i < n ? zc[i] : 0.0;
+    self = fma(zv[k], zv[k], self);
+  }
+  double* pc = partials + (long long)c * nb * width;
+  __shared__ double s_self[VEC_THREADS / 32];
+  self = warp_sum(self);
+  if ((threadIdx.x & 31) == 0) s_self[threadIdx.x >> 5] = self;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < VEC_THREADS / 32; ++w) t += s_self[w];
+    pc[(long long)blockIdx.x * width] = t;
+  }
+  block_dots<VEC_ROWS>(zv, rows, n, V + (long long)c * ldcol, ldv, nv, pc, width, 1, nullptr);
+}
+
+int launch_dots_batch(int n, const double* z, long long ldz, const double* V, long long ldv, long long ldcol,
+                      int nv, const ColList& cols, double* partials, int width, int* nb_out, cudaStream_t st) {
+  const int nb = ceil_div(n, VEC_TILE);
+  if (nb_out) *nb_out = nb;
+  if (n == 0 || cols.n == 0) return HG_OK;
+  k_dots_batch<<<dim3(nb, cols.n), VEC_THREADS, 0, st>>>(n, z, ldz, V, ldv, ldcol, nv, cols, partials, width, nb);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+__global__ void __launch_bounds__(256) k_reduce_batch(const double* __restrict__ partials, int nb, int width,
+                                                      ColList cols, double* __restrict__ out, long long ow) {
+  __shared__ double s[256];
+  const int k = blockIdx.x, c = cols.c[blockIdx.y];
+  const double* pc = partials + (long long)c * nb * width;
+  double t = 0.0;
+  for (int b = threadIdx.x; b < nb; b += 256) t += pc[(long long)b * width + k];
+  s[threadIdx.x] = t;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[(long long)c * ow + k] = s[0];
+}
+
+int launch_reduce_batch(const double* partials, int nb, int width, int cnt, const ColList& cols, double* out,
+                        long long ow, cudaStream_t st) {
+  if (cnt == 0 || cols.n == 0) return HG_OK;
+  k_reduce_batch<<<dim3(cnt, cols.n), 256, 0, st>>>(partials, nb, width, cols, out, ow);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+__global__ void __launch_bounds__(VEC_THREADS) k_axpy_batch(int n, double* __restrict__ w, long long ldw,
+                                                            const double* __restrict__ V, long long ldv,
+                                                            long long ldcol, int nv, const double* __restrict__ coef,
+                                                            long long ldcoef, int mode, ColList cols) {
+  __shared__ double s_coef[MAX_NV];
+  const int c = cols.c[blockIdx.y];
+  const double* cc = coef + (long long)c * ldcoef;
+  for (int i = threadIdx.x; i < nv; i += VEC_THREADS) s_coef[i] = cc[i];
+  __syncthreads();
+  double* wc = w + (long long)c * ldw;
+  const double* Vc = V + (long long)c * ldcol;
+#pragma unroll
+  for (int k = 0; k < VEC_ROWS; ++k) {
+    const int d = blockIdx.x * VEC_TILE + k * VEC_THREADS + threadIdx.x;
+    if (d >= n) continue;
+    double acc = mode ? wc[d] : 0.0;
+    if (mode == 1) {
+      for (int i = 0; i < nv; ++i) acc = fma(-s_coef[i], __ldg(Vc + (long long)i * ldv + d), acc);
+    } else {
+      for (int i = 0; i < nv; ++i) acc = fma(s_coef[i], __ldg(Vc + (long long)i * ldv + d), acc);
+    }
+    wc[d] = acc;
+  }
+}
+
+int launch_axpy_batch(int n, double* w, long long ldw, const double* V, long long ldv, long long ldcol, int nv,
+                      const double* coef, long long ldcoef, int mode, const ColList& cols, cudaStream_t st) {
+  if (n == 0 || cols.n == 0) return HG_OK;
+  if (nv > MAX_NV) {
+    set_error("axpy_batch: more than 1024 basis vectors");
+    return HG_ERR_UNSUPPORTED;
+  }
+  k_axpy_batch<<<dim3(ceil_div(n, VEC_TILE), cols.n), VEC_THREADS, 0, st>>>(n, w, ldw, V, ldv, ldcol, nv, coef,
+                                                                             ldcoef, mode, cols);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+__global__ void k_scale_batch(int n, const double* __restrict__ w, const double* __restrict__ ww, long long ldw,
+                              double* __restrict__ V, double* __restrict__ WV, long long ldcol, ColList cols) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  const int c = cols.c[blockIdx.y];
+  const double h = cols.s[blockIdx.y];
+  V[(long long)c * ldcol + d] = w[(long long)c * ldw + d] / h;
+  if (WV) WV[(long long)c * ldcol + d] = ww[(long long)c * ldw + d] / h;
+}
+
+int launch_scale_batch(int n, const double* w, const double* ww, long long ldw, double* V, double* WV,
+                       long long ldcol, const ColList& cols, cudaStream_t st) {
+  if (n == 0 || cols.n == 0) return HG_OK;
+  k_scale_batch<<<dim3(ceil_div(n, 256), cols.n), 256, 0, st>>>(n, w, ww, ldw, V, WV, ldcol, cols);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+__global__ void k_fill_batch(int n, double* __restrict__ y, long long ldy, ColList cols) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d < n) y[(long long)cols.c[blockIdx.y] * ldy + d] = 0.0;
+}
+
+int launch_fill_batch(int n, double* y, long long ldy, const ColList& cols, cudaStream_t st) {
+  if (n == 0 || cols.n == 0) return HG_OK;
+  k_fill_batch<<<dim3(ceil_div(n, 256), cols.n), 256, 0, st>>>(n, y, ldy, cols);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+// ------------------------------------------------------------------ scratch
+int multi_prepare(HgPrecond* P) {
+  if (P->multi_ready) return HG_OK;
+  auto alloc = [&](double** p, size_t count) -> int {
+    if (count == 0) count = 1;
+    HG_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(p), sizeof(double) * count));
+    P->device_bytes += (long long)(sizeof(double) * count);
+    return HG_OK;
+  };
+  HG_TRY(alloc(&P->d_xsm, (size_t)MR * P->xs_len));
+  HG_TRY(alloc(&P->d_tmpm, (size_t)MR * P->n));
+  if (P->m > 0) {
+    HG_TRY(alloc(&P->d_zsm, (size_t)MR * P->zs_len));
+    HG_TRY(alloc(&P->d_cpartm, (size_t)MR * P->part_len));
+    HG_TRY(alloc(&P->d_ym, (size_t)MR * P->m));
+    HG_TRY(alloc(&P->d_b0m_x, (size_t)2 * P->b0_K * BP * MR));
+    HG_CUDA_TRY(cudaMalloc(&P->d_b0m_done, sizeof(unsigned long long)));
+    HG_CUDA_TRY(cudaMemset(P->d_b0m_done, 0, sizeof(unsigned long long)));
+    P->b0m_epoch = 0;
+  }
+  HG_CUDA_TRY(cudaDeviceSynchronize());
+  P->multi_ready = true;
+  return HG_OK;
+}
+
+int preload_multi() {
+  cudaFuncAttributes at;
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_spmm));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_zt_multi));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_zy_multi));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_b0_multi));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_assemble_multi));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_dots_batch));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_reduce_batch));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_axpy_batch));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_scale_batch));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_fill_batch));
+  return HG_OK;
+}
+
+}  // namespace hg
+
+// ------------------------------------------------------------------ DCGS2 Arnoldi kernels
+namespace hg {
+
+// Butterfly reduce-scatter of 16 per-lane values over a warp: afterwards
+// lane L holds the warp total of value ((L>>4)&1)*8 + ((L>>3)&1)*4 +
+// ((L>>2)&1)*2 + ((L>>1)&1) (16 shuffles instead of 16 x 5).
+__device__ __forceinline__ double warp_reduce16(double (&v)[16], int lane) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool hi = lane & 16;
+    const double send = hi ? v[i] : v[8 + i];
+    const double keep = hi ? v[8 + i] : v[i];
+    v[i] = keep + __shfl_xor_sync(FULL, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool hi = lane & 8;
+    const double send = hi ? v[i] : v[4 + i];
+    const double keep = hi ? v[4 + i] : v[i];
+    v[i] = keep + __shfl_xor_sync(FULL, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool hi = lane & 4;
+    const double send = hi ? v[i] : v[2 + i];
+    const double keep = hi ? v[2 + i] : v[i];
+    v[i] = keep + __shfl_xor_sync(FULL, send, 4);
+  }
+  {
+    const bool hi = lane & 2;
+    const double send = hi ? v[0] : v[1];
+    const double keep = hi ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(FULL, send, 2);
+  }
+  return v[0] + __shfl_xor_sync(FULL, v[0], 1);
+}
+
+// 8-value variant: lane L ends with the total of value ((L>>4)&1)*4 + ((L>>3)&1)*2 + ((L>>2)&1).
+__device__ __forceinline__ double warp_reduce8(double (&v)[8], int lane) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool hi = lane & 16;
+    const double send = hi ? v[i] : v[4 + i];
+    const double keep = hi ? v[4 + i] : v[i];
+    v[i] = keep + __shfl_xor_sync(FULL, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool hi = lane & 8;
+    const double send = hi ? v[i] : v[2 + i];
+    const double keep = hi ? v[2 + i] : v[i];
+    v[i] = keep + __shfl_xor_sync(FULL, send, 8);
+  }
+  {
+    const bool hi = lane & 4;
+    const double send = hi ? v[0] : v[1];
+    const double keep = hi ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(FULL, send, 4);
+  }
+  double t = v[0] + __shfl_xor_sync(FULL, v[0], 2);
+  return t + __shfl_xor_sync(FULL, t, 1);
+}
+
+constexpr int D2_CH = 4;  // basis vectors per chunk: 8 sums (4 . a, 4 . u) per lane
+
+// Column c: dots of its basis V_c[0..nv) with a_c and u_c, each V_i read once.
+// A thread owns VEC_ROWS rows; a chunk of 4 vectors issues all 16 loads
+// before any reduction; per-warp totals by warp_reduce8, per-block totals
+// in a fixed order through a double-buffered smem slot (one barrier per
+// chunk).  partials value-major: [(c * width + k) * nb + block], k < 2 nv
+// (k < nv: V_k . a, nv + k: V_k . u).
+__global__ void __launch_bounds__(VEC_THREADS, 3) k_dots2_batch(int n, const double* __restrict__ A, long long lda,
+                                                             const double* __restrict__ U, long long ldu,
+                                                             const double* __restrict__ V, long long ldv,
+                                                             long long ldcol, int nv, ColList cols,
+                                                             double* __restrict__ partials, int width, int nb) {
+  __shared__ double s_p[2][VEC_THREADS / 32][2 * D2_CH];
+  const int c = cols.c[blockIdx.y];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double av[VEC_ROWS], uv[VEC_ROWS];
+  int rows[VEC_ROWS];
+#pragma unroll
+  for (int k = 0; k < VEC_ROWS; ++k) {
+    const int i = blockIdx.x * VEC_TILE + k * VEC_THREADS + threadIdx.x;
+    rows[k] = i < n ? i : -1;
+    av[k] = i < n ? A[(long long)c * lda + i] : 0.0;
+    uv[k] = i < n ? U[(long long)c * ldu + i] : 0.0;
+  }
+  const double* Vc = V + (long long)c * ldcol;
+  double* pc = partials + (long long)c * width * nb;
+  const int my = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  int buf = 0;
+  for (int i0 = 0; i0 < nv; i0 += D2_CH, buf ^= 1) {
+    double x[D2_CH][VEC_ROWS];
+#pragma unroll
+    for (int t = 0; t < D2_CH; ++t)
+#pragma unroll
+      for (int k = 0; k < VEC_ROWS; ++k)
+        x[t][k] = (i0 + t < nv && rows[k] >= 0) ? __ldg(Vc + (long long)(i0 + t) * ldv + rows[k]) : 0.0;
+    double v[2 * D2_CH];
+#pragma unroll
+    for (int t = 0; t < D2_CH; ++t) {
+      double pa = 0.0, pu = 0.0;
+#pragma unroll
+      for (int k = 0; k < VEC_ROWS; ++k) {
+        pa = fma(x[t][k], av[k], pa);
+        pu = fma(x[t][k], uv[k], pu);
+      }
+      v[t] = pa;
+      v[D2_CH + t] = pu;
+    }
+    const double tot = warp_reduce8(v, lane);
+    if (!(lane & 3)) s_p[buf][warp][my] = tot;
+    __syncthreads();
+    if (threadIdx.x < 2 * D2_CH) {
+      const int t = threadIdx.x % D2_CH, which = threadIdx.x / D2_CH;
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < VEC_THREADS / 32; ++w) sum += s_p[buf][w][threadIdx.x];
+      if (i0 + t < nv) pc[(long long)(which * nv + i0 + t) * nb + blockIdx.x] = sum;
+    }
+  }
+}
+
+// out[c * ow + k] = sum_b partials[(c * width + k) * nb + b] (contiguous, fixed order)
+__global__ void __launch_bounds__(256) k_reduce_vm(const double* __restrict__ partials, int nb, int width,
+                                                   ColList cols, double* __restrict__ out, long long ow) {
+  __shared__ double s[256];
+  const int k = blockIdx.x, c = cols.c[blockIdx.y];
+  const double* p = partials + ((long long)c * width + k) * nb;
+  double t = 0.0;
+  for (int b = threadIdx.x; b < nb; b += 256) t += p[b];
+  s[threadIdx.x] = t;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[(long long)c * ow + k] = s[0];
+}
+
+int launch_dots2_batch(int n, const double* A, long long lda, const double* U, long long ldu, const double* V,
+                       long long ldv, long long ldcol, int nv, const ColList& cols, double* partials, double* out,
+                       long long ow, cudaStream_t st) {
+  const int nb = ceil_div(n, VEC_TILE);
+  if (n == 0 || cols.n == 0) return HG_OK;
+  k_dots2_batch<<<dim3(nb, cols.n), VEC_THREADS, 0, st>>>(n, A, lda, U, ldu, V, ldv, ldcol, nv, cols, partials,
+                                                          2 * nv, nb);
+  HG_LAUNCH_CHECK();
+  k_reduce_vm<<<dim3(2 * nv, cols.n), 256, 0, st>>>(partials, nb, 2 * nv, cols, out, ow);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+// Delayed reorthogonalisation + projection in one read of V_c[0..j):
+//   q  = (V_c[j] - sum_{i<j} s_i V_c[i]) * rinv          (q_j re-orthogonalised)
+//   w  = w * rinv - sum_{i<j} c_i V_c[i] - c_j q          (w projected)
+// coef row of column c: [rinv, s_0..s_{j-1}, c_0..c_j].
+__global__ void __launch_bounds__(VEC_THREADS) k_dcgs2_update(int n, double* __restrict__ V, long long ldv,
+                                                              long long ldcol, int j, double* __restrict__ w,
+                                                              long long ldw, const double* __restrict__ coef,
+                                                              long long ldcoef, ColList cols) {
+  __shared__ double s_c[2 * MAX_NV + 2];
+  const int c = cols.c[blockIdx.y];
+  const double* cc = coef + (long long)c * ldcoef;
+  for (int i = threadIdx.x; i < 2 * j + 2; i += VEC_THREADS) s_c[i] = cc[i];
+  __syncthreads();
+  const double rinv = s_c[0];
+  const double* sv = s_c + 1;
+  const double* cv = s_c + 1 + j;
+  double* Vc = V + (long long)c * ldcol;
+  double* wc = w + (long long)c * ldw;
+  double aq[VEC_ROWS], aw[VEC_ROWS];
+  int rows[VEC_ROWS];
+#pragma unroll
+  for (int k = 0; k < VEC_ROWS; ++k) {
+    const int d = blockIdx.x * VEC_TILE + k * VEC_THREADS + threadIdx.x;
+    rows[k] = d < n ? d : -1;
+    aq[k] = d < n ? Vc[(long long)j * ldv + d] : 0.0;
+    aw[k] = d < n ? wc[d] * rinv : 0.0;
+  }
+#pragma unroll 4
+  for (int i = 0; i < j; ++i) {  // sequential in i per row: fixed summation order
+    const double* vi = Vc + (long long)i * ldv;
+    const double si = sv[i], ci = cv[i];
+#pragma unroll
+    for (int k = 0; k < VEC_ROWS; ++k) {
+      const double x = rows[k] >= 0 ? __ldg(vi + rows[k]) : 0.0;
+      aq[k] = fma(-si, x, aq[k]);
+      aw[k] = fma(-ci, x, aw[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < VEC_ROWS; ++k) {
+    if (rows[k] < 0) continue;
+    const double qn = aq[k] * rinv;
+    Vc[(long long)j * ldv + rows[k]] = qn;
+    wc[rows[k]] = fma(-cv[j], qn, aw[k]);
+  }
+}
+
+int launch_dcgs2_update(int n, double* V, long long ldv, long long ldcol, int j, double* w, long long ldw,
+                        const double* coef, long long ldcoef, const ColList& cols, cudaStream_t st) {
+  if (n == 0 || cols.n == 0) return HG_OK;
+  if (j + 1 > MAX_NV) {
+    set_error("dcgs2 update: more than 1024 basis vectors");
+    return HG_ERR_UNSUPPORTED;
+  }
+  k_dcgs2_update<<<dim3(ceil_div(n, VEC_TILE), cols.n), VEC_THREADS, 0, st>>>(n, V, ldv, ldcol, j, w, ldw, coef,
+                                                                               ldcoef, cols);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+// V_c = w_c / h_c and (WQ) Wq_c = ww_c / h_c with h_c = sqrt(max(nrm2[c], 0))
+// read on the device (no host round trip before the next operator apply).
+__global__ void k_scale_dev_batch(int n, const double* __restrict__ w, const double* __restrict__ ww, long long ldw,
+                                  double* __restrict__ V, long long ldcol, double* __restrict__ Wq,
+                                  const double* __restrict__ nrm2, ColList cols) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= n) return;
+  const int c = cols.c[blockIdx.y];
+  const double h = sqrt(fmax(nrm2[c], 0.0));
+  V[(long long)c * ldcol + d] = w[(long long)c * ldw + d] / h;
+  if (Wq) Wq[(long long)c * ldw + d] = ww[(long long)c * ldw + d] / h;
+}
+
+int launch_scale_dev_batch(int n, const double* w, const double* ww, long long ldw, double* V, long long ldcol,
+                           double* Wq, const double* nrm2, const ColList& cols, cudaStream_t st) {
+  if (n == 0 || cols.n == 0) return HG_OK;
+  k_scale_dev_batch<<<dim3(ceil_div(n, 256), cols.n), 256, 0, st>>>(n, w, ww, ldw, V, ldcol, Wq, nrm2, cols);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+int preload_dcgs2() {
+  cudaFuncAttributes at;
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_dots2_batch));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_reduce_vm));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_dcgs2_update));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_scale_dev_batch));
+  return HG_OK;
+}
+
+}  // namespace hg
+
+namespace hg {
+__global__ void k_add(int n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out) {
+  const int d = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d < n) out[d] = a[d] + b[d];
+}
+
+int launch_add(int n, const double* a, const double* b, double* out, cudaStream_t st) {
+  if (n == 0) return HG_OK;
+  k_add<<<ceil_div(n, 256), 256, 0, st>>>(n, a, b, out);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+int preload_add() {
+  cudaFuncAttributes at;
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_add));
+  return HG_OK;
+}
+}  // namespace hg

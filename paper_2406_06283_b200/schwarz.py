@@ -62,6 +62,41 @@ def _vp(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _as_device_batch(V, n):
+    """(device tensor of shape (nrhs, n), was_numpy) for a batch of vectors.
+
+    numpy input is an (n, nrhs) matrix (scipy's column convention; 1-D =
+    one column); a CUDA tensor is taken as (nrhs, n) — column c contiguous,
+    i.e. a column-major (n, nrhs) matrix — which is the device layout."""
+    torch = _torch()
+    if isinstance(V, torch.Tensor):
+        t = V.detach()
+        if t.device.type != "cuda":
+            t = t.cuda()
+        t = t.to(torch.float64)
+        if t.ndim == 1:
+            t = t.reshape(1, -1)
+        t = t.contiguous()
+        if t.shape[1] != n:
+            raise ValueError("batch has vectors of length %d, operator has %d" % (t.shape[1], n))
+        was_np = False
+    else:
+        a = np.asarray(V, dtype=np.float64)
+        if a.ndim == 1:
+            a = a[:, None]
+        if a.shape[0] != n:
+            raise ValueError("batch has %d rows, operator has %d" % (a.shape[0], n))
+        t = torch.from_numpy(np.ascontiguousarray(a.T)).cuda()
+        was_np = True
+    if not 1 <= t.shape[0] <= _lib.MAX_RHS:
+        raise ValueError("batch of %d columns; 1..%d supported per call" % (t.shape[0], _lib.MAX_RHS))
+    return t, was_np
+
+
+def _from_device_batch(t, was_np):
+    return t.cpu().numpy().T.copy() if was_np else t
+
+
 class GpuBandLU:
     """``LocalSolver.lu`` stand-in: ``solve`` runs the device band solve of
     one block (hg_local_solve); the host factors stay available for tests."""
@@ -350,6 +385,32 @@ class TwoLevelPreconditioner:
         """M^{-1} r (schwarz.py:51-61); returns a new array."""
         return self._run("hg_precond_apply", r)
 
+    def apply_multi(self, R):
+        """M^{-1} applied to every column of R in ONE batched apply (SURVEY §8a
+        row a15; column c equals ``apply(R[:, c])`` to rounding).  numpy R is
+        (n, nrhs); a CUDA tensor is (nrhs, n) and the result stays on device."""
+        torch = _torch()
+        t, was_np = _as_device_batch(R, self.n)
+        out = torch.empty_like(t)
+        _lib.check(
+            _lib.load().hg_precond_apply_multi(self._handle, _vp(t), self.n, _vp(out), self.n, t.shape[0], _stream()),
+            "hg_precond_apply_multi",
+        )
+        return _from_device_batch(out, was_np)
+
+    def profile_multi(self, R, iters=5):
+        """Mean device ms per stage of the batched apply (stages serialised)."""
+        torch = _torch()
+        t, _ = _as_device_batch(R, self.n)
+        out = torch.empty_like(t)
+        ms = np.zeros(len(self.STAGES))
+        _lib.check(
+            _lib.load().hg_precond_profile_multi(self._handle, _vp(t), self.n, _vp(out), self.n, t.shape[0],
+                                                 int(iters), _lib.ptr(ms, ctypes.c_double), _stream()),
+            "hg_precond_profile_multi",
+        )
+        return dict(zip(self.STAGES, ms.tolist()))
+
     def apply_T(self, u):
         """T u = M^{-1} B u (schwarz.py:63-65)."""
         return self._run("hg_precond_apply_T", u)
@@ -411,6 +472,31 @@ class TwoLevelPreconditioner:
         rep.reorth_passes = int(info[3])
         return x, rep
 
+    def solve_host_batch(self, F, rtol=1e-6, maxit=200):
+        """Batched end-to-end solve through the C ABI with host buffers
+        (hg_solve_host_batch): F is (n, nrhs); returns (X, [GmresReport])."""
+        from .wgmres import _reports
+
+        F = np.asarray(F, dtype=np.float64)
+        if F.ndim == 1:
+            F = F[:, None]
+        nrhs = F.shape[1]
+        if not 1 <= nrhs <= _lib.MAX_RHS:
+            raise ValueError("batch of %d columns; 1..%d supported per call" % (nrhs, _lib.MAX_RHS))
+        Fc = np.ascontiguousarray(F.T)
+        Xc = np.empty_like(Fc)
+        maxit = int(min(maxit, self.n))
+        hist = np.zeros((nrhs, maxit + 1))
+        info = np.zeros((nrhs, 4), dtype=np.int32)
+        _lib.check(
+            _lib.load().hg_solve_host_batch(
+                self._handle, _lib.ptr(Fc, ctypes.c_double), _lib.ptr(Xc, ctypes.c_double), nrhs, float(rtol),
+                maxit, _lib.ptr(hist, ctypes.c_double), _lib.ptr(info, ctypes.c_int32), _stream(),
+            ),
+            "hg_solve_host_batch",
+        )
+        return Xc.T.copy(), _reports(hist, info, None)
+
     def close(self):
         if self._handle is not None:
             _lib.load().hg_precond_destroy(self._handle)
@@ -440,6 +526,17 @@ class DeviceOperator:
         out = torch.empty_like(t)
         _lib.check(_lib.load().hg_op_apply(self._handle, _vp(t), _vp(out), _stream()), "hg_op_apply")
         return out.cpu().numpy() if was_np else out
+
+    def apply_multi(self, V):
+        """op applied to every column of a batch (numpy (n, nrhs) or CUDA (nrhs, n))."""
+        torch = _torch()
+        t, was_np = _as_device_batch(V, self.n)
+        out = torch.empty_like(t)
+        _lib.check(
+            _lib.load().hg_op_apply_multi(self._handle, _vp(t), self.n, _vp(out), self.n, t.shape[0], _stream()),
+            "hg_op_apply_multi",
+        )
+        return _from_device_batch(out, was_np)
 
     def __del__(self):
         try:
@@ -480,6 +577,17 @@ class CsrOperator:
         out = torch.empty_like(t)
         _lib.check(_lib.load().hg_op_apply(self._handle, _vp(t), _vp(out), _stream()), "hg_op_apply")
         return out.cpu().numpy() if was_np else out
+
+    def apply_multi(self, V):
+        """op applied to every column of a batch (numpy (n, nrhs) or CUDA (nrhs, n))."""
+        torch = _torch()
+        t, was_np = _as_device_batch(V, self.n)
+        out = torch.empty_like(t)
+        _lib.check(
+            _lib.load().hg_op_apply_multi(self._handle, _vp(t), self.n, _vp(out), self.n, t.shape[0], _stream()),
+            "hg_op_apply_multi",
+        )
+        return _from_device_batch(out, was_np)
 
     def __del__(self):
         try:

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for name in _declared():
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, name
-    assert lib.hg_abi_version() == 1
+    assert lib.hg_abi_version() == _lib.ABI_VERSION
     assert lib.hg_last_error() == b""
 
 

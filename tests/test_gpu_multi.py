@@ -1,0 +1,194 @@
+"""Multi-RHS (batched) solve phase, SURVEY §8a row a15 (BASELINE config 5's
+16 right-hand sides as one block).  There is no reference function for a
+batch: every column is checked against the one-at-a-time device path (itself
+pinned to the reference's golden vectors in test_gpu_parity.py) and, where
+cheap, against the CPU oracle / the reference's golden values directly.
+Bars: apply columns rel <= 1e-12 vs the single apply (1e-10 vs the reference),
+SpMM bitwise, GMRES iterations +-1 and solution rel <= 1e-8 per column."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import paper_2406_06283_b200 as hg
+from _helpers import golden_coarse
+from oracle.schwarz_oracle import OraclePreconditioner
+from oracle.wgmres_oracle import weighted_gmres as oracle_gmres
+
+pytestmark = pytest.mark.gpu
+
+APPLY_RTOL = 1e-10
+SOL_RTOL = 1e-8
+
+
+def rel(a, b):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def colrel(A, B):
+    return max(rel(A[:, c], B[:, c]) for c in range(B.shape[1]))
+
+
+@pytest.fixture(scope="module")
+def cfg1(golden):
+    g = golden("config1")
+    P = hg.build_problem("1", workers=1, one_level=True)
+    coarse = golden_coarse(g, P.forms.n_dofs)
+    pre = hg.factorize(P.forms, P.dec, coarse)
+    return P, g, coarse, pre
+
+
+def test_spmm_bitwise(cfg1):
+    P, g, _, pre = cfg1
+    U = np.random.default_rng(3).standard_normal((pre.n, 16))
+    U[:, 0] = g["u"]
+    for kind, M in (("B", pre._B), ("Dk", pre._Dk)):
+        got = pre.as_operator(kind).apply_multi(U)
+        for c in range(16):
+            assert np.array_equal(got[:, c], M @ U[:, c]), (kind, c)
+    assert np.array_equal(pre.as_operator("B").apply_multi(U)[:, 0], g["Bu"])
+
+
+@pytest.mark.parametrize("nrhs", [1, 3, 16])
+def test_apply_multi_matches_single(cfg1, nrhs):
+    P, g, _, pre = cfg1
+    R = np.random.default_rng(nrhs).standard_normal((pre.n, nrhs))
+    R[:, 0] = g["r"]
+    got = pre.apply_multi(R)
+    want = np.stack([pre.apply(R[:, c]) for c in range(nrhs)], axis=1)
+    assert colrel(got, want) <= 1e-12
+    assert rel(got[:, 0], g["apply_r"]) <= APPLY_RTOL  # the reference's own value
+    # deterministic, and the batched operator T = M^-1 B too
+    assert np.array_equal(pre.apply_multi(R), got)
+    T = pre.as_operator("T").apply_multi(R)
+    assert colrel(T, np.stack([pre.apply_T(R[:, c]) for c in range(nrhs)], axis=1)) <= 1e-12
+
+
+def test_apply_multi_zero_columns_and_device_tensors(cfg1):
+    import torch
+
+    _, g, _, pre = cfg1
+    R = np.zeros((pre.n, 4))
+    R[:, 2] = g["r"]
+    got = pre.apply_multi(R)
+    assert np.all(got[:, [0, 1, 3]] == 0.0)
+    assert rel(got[:, 2], g["apply_r"]) <= APPLY_RTOL
+    t = torch.from_numpy(np.ascontiguousarray(R.T)).cuda()
+    out = pre.apply_multi(t)
+    assert isinstance(out, torch.Tensor) and out.is_cuda and tuple(out.shape) == (4, pre.n)
+    assert np.array_equal(out.cpu().numpy().T, got)
+    with pytest.raises(ValueError):
+        pre.apply_multi(np.zeros((pre.n, 17)))
+
+
+def test_apply_multi_one_level(cfg1):
+    P, g, _, _ = cfg1
+    pre1 = hg.factorize(P.forms, P.dec, None)
+    R = np.random.default_rng(5).standard_normal((pre1.n, 5))
+    R[:, 1] = g["r"]
+    got = pre1.apply_multi(R)
+    assert rel(got[:, 1], g["apply_one_level_r"]) <= APPLY_RTOL
+    want = np.stack([pre1.apply(R[:, c]) for c in range(5)], axis=1)
+    assert np.array_equal(got, want)  # no coarse part: same kernels, same order, bitwise
+
+
+def test_apply_multi_unpremultiplied_coarse_tiles(cfg1, monkeypatch):
+    """The batched coarse solve on the L2-counter tile layout (b0 mode 0)."""
+    P, g, coarse, _ = cfg1
+    monkeypatch.setenv("HG_B0_MODE", "0")
+    pre0 = hg.factorize(P.forms, P.dec, coarse)
+    assert pre0.b0_mode == 0
+    R = np.random.default_rng(9).standard_normal((pre0.n, 16))
+    R[:, 5] = g["r"]
+    got = pre0.apply_multi(R)
+    want = np.stack([pre0.apply(R[:, c]) for c in range(16)], axis=1)
+    assert colrel(got, want) <= 1e-12
+    assert rel(got[:, 5], g["apply_r"]) <= APPLY_RTOL
+
+
+@pytest.mark.parametrize("orth", ["dcgs2", "measured"])
+def test_gmres_batch_matches_single_and_reference(cfg1, orth):
+    P, g, _, pre = cfg1
+    rng = np.random.default_rng(21)
+    F = rng.standard_normal((pre.n, 6))
+    F[:, 0] = P.rhs
+    F[:, 3] = 0.0  # zero right-hand side: 0 iterations, x = 0
+    Rp = pre.apply_multi(F)
+    X, reps = hg.weighted_gmres_batch(pre.as_operator("T"), Rp, weight=P.forms.dk, rtol=1e-6, maxit=1000, orth=orth)
+    assert len(reps) == 6
+    assert reps[3].iterations == 0 and reps[3].converged and np.all(X[:, 3] == 0.0)
+    assert abs(reps[0].iterations - int(g["iterations"])) <= 1
+    assert rel(X[:, 0], g["x"]) <= SOL_RTOL
+    for c in (0, 1, 2, 4, 5):
+        x, rep = hg.weighted_gmres(pre.as_operator("T"), Rp[:, c], weight=P.forms.dk, rtol=1e-6, maxit=1000,
+                                   orth=orth)
+        assert rep.converged and reps[c].converged
+        assert abs(rep.iterations - reps[c].iterations) <= 1
+        assert rel(X[:, c], x) <= SOL_RTOL
+        k = min(rep.residual_history.size, reps[c].residual_history.size)
+        assert np.abs(rep.residual_history[:k] - reps[c].residual_history[:k]).max() <= 1e-8 * rep.residual_history[0]
+
+
+@pytest.mark.parametrize("orth", ["dcgs2", "measured"])
+def test_gmres_batch_fixed_iterations_and_maxit(cfg1, orth):
+    P, g, _, pre = cfg1
+    F = np.random.default_rng(4).standard_normal((pre.n, 3))
+    F[:, 1] = P.rhs
+    Rp = pre.apply_multi(F)
+    it = int(g["iterations"])
+    X, reps = hg.weighted_gmres_batch(pre.as_operator("T"), Rp, weight=P.forms.dk, rtol=0.0, maxit=it, orth=orth)
+    assert all(r.iterations == it and not r.converged for r in reps)
+    assert rel(X[:, 1], g["x_fixed"]) <= SOL_RTOL
+
+
+@pytest.mark.parametrize("orth", ["dcgs2", "measured"])
+def test_gmres_batch_seeded_systems(golden, orth):
+    g = golden("wgmres")
+    B = np.stack([g["b30"], np.roll(g["b30"], 3), -2.0 * g["b30"]], axis=1)
+    for m in (5, 12, 25):
+        X, reps = hg.weighted_gmres_batch(g["A30"], B, rtol=0.0, maxit=m, orth=orth)
+        assert all(r.iterations == m for r in reps)
+        assert np.abs(X[:, 0] - g["x30_%d" % m]).max() <= 1e-10 * max(np.abs(g["x30_%d" % m]).max(), 1.0)
+        assert np.abs(reps[0].residual_history - g["h30_%d" % m]).max() <= 1e-10 * g["h30_%d" % m][0]
+        assert np.abs(X[:, 2] + 2.0 * X[:, 0]).max() <= 1e-10 * np.abs(X[:, 0]).max()
+    W = sp.csr_matrix(g["W50"])
+    X, reps = hg.weighted_gmres_batch(g["A50"], np.stack([g["b50"], g["b50"]], axis=1), weight=W, rtol=1e-10,
+                                      maxit=50, orth=orth)
+    for c in range(2):
+        assert reps[c].converged and abs(reps[c].iterations - int(g["it50"])) <= (0 if orth == "measured" else 1)
+        assert rel(X[:, c], g["x50"]) <= 1e-10
+
+
+def test_solve_host_batch(cfg1):
+    P, g, _, pre = cfg1
+    F = np.random.default_rng(6).standard_normal((pre.n, 4))
+    F[:, 2] = P.rhs
+    X, reps = pre.solve_host_batch(F, rtol=1e-6, maxit=1000)
+    assert abs(reps[2].iterations - int(g["iterations"])) <= 1
+    assert rel(X[:, 2], g["x"]) <= SOL_RTOL
+    x, rep = pre.solve_host(F[:, 0], rtol=1e-6, maxit=1000)
+    assert abs(rep.iterations - reps[0].iterations) <= 1 and rel(X[:, 0], x) <= SOL_RTOL
+
+
+@pytest.mark.parametrize("name", ["2", "3"])
+def test_config_batch_parity_vs_oracle(name):
+    """Multi-CTA batched coarse solve (K = 40 / 4 panels) against the oracle."""
+    P = hg.build_problem(name)
+    pre = hg.factorize(P.forms, P.dec, P.coarse)
+    orc = OraclePreconditioner(P.forms, P.dec, P.coarse)
+    R = np.random.default_rng(12).standard_normal((P.forms.n_dofs, 16))
+    got = pre.apply_multi(R)
+    for c in (0, 7, 15):
+        assert rel(got[:, c], orc.apply(R[:, c])) <= APPLY_RTOL
+    want = np.stack([pre.apply(R[:, c]) for c in range(16)], axis=1)
+    assert colrel(got, want) <= 1e-12
+    B, Dk = P.forms.helmholtz, P.forms.dk
+    F = np.stack([P.rhs, R[:, 1]], axis=1)
+    X, reps = hg.weighted_gmres_batch(pre.as_operator("T"), pre.apply_multi(F), weight=Dk, rtol=1e-6, maxit=1000)
+    for c in range(2):
+        xo, info = oracle_gmres(lambda v: orc.apply(B @ v), orc.apply(F[:, c]), weight=Dk, rtol=1e-6, maxit=1000)
+        assert reps[c].converged and info["converged"]
+        assert abs(reps[c].iterations - info["iterations"]) <= 1
+        assert rel(X[:, c], xo) <= SOL_RTOL

@@ -99,11 +99,15 @@ def test_local_solves_match_lapack(cfg1):
         assert rel(got, want) <= 1e-12
 
 
-def test_gmres_matches_reference(cfg1):
+ORTHS = ["dcgs2", "measured"]
+
+
+@pytest.mark.parametrize("orth", ORTHS)
+def test_gmres_matches_reference(cfg1, orth):
     P, g, _, pre = cfg1
     rhs_p = pre.apply(P.rhs)
     assert rel(rhs_p, g["rhs_p"]) <= APPLY_RTOL
-    x, rep = hg.weighted_gmres(pre.as_operator("T"), rhs_p, weight=P.forms.dk, rtol=1e-6, maxit=1000)
+    x, rep = hg.weighted_gmres(pre.as_operator("T"), rhs_p, weight=P.forms.dk, rtol=1e-6, maxit=1000, orth=orth)
     assert rep.converged
     assert abs(rep.iterations - int(g["iterations"])) <= 1
     assert rel(x, g["x"]) <= SOL_RTOL
@@ -112,7 +116,7 @@ def test_gmres_matches_reference(cfg1):
     assert np.abs(rep.residual_history[:k] - h[:k]).max() <= 1e-8 * h[0]
     # fixed-iteration mode: no stopping-rule slack can hide drift
     xf, repf = hg.weighted_gmres(pre.as_operator("T"), rhs_p, weight=P.forms.dk, rtol=0.0,
-                                 maxit=int(g["iterations"]))
+                                 maxit=int(g["iterations"]), orth=orth)
     assert repf.iterations == int(g["iterations"])
     assert rel(xf, g["x_fixed"]) <= SOL_RTOL
 
@@ -124,10 +128,12 @@ def test_solve_host_end_to_end(cfg1):
     assert rel(x, g["x"]) <= SOL_RTOL
 
 
-def test_one_level_gmres_iterations(cfg1, golden):
+@pytest.mark.parametrize("orth", ORTHS)
+def test_one_level_gmres_iterations(cfg1, golden, orth):
     P, g, _, _ = cfg1
     pre1 = hg.factorize(P.forms, P.dec, None)
-    x, rep = hg.weighted_gmres(pre1.as_operator("T"), pre1.apply(P.rhs), weight=P.forms.dk, rtol=1e-6, maxit=1000)
+    x, rep = hg.weighted_gmres(pre1.as_operator("T"), pre1.apply(P.rhs), weight=P.forms.dk, rtol=1e-6, maxit=1000,
+                               orth=orth)
     assert abs(rep.iterations - int(g["iterations_one_level"])) <= 1
     assert rel(x, g["x_one_level"]) <= SOL_RTOL
 
@@ -156,15 +162,16 @@ def test_small_pipelines(golden):
     assert rel(got, g["deg_apply_Bv"]) <= 1e-10
 
 
-def test_gmres_seeded_systems(golden):
+@pytest.mark.parametrize("orth", ORTHS)
+def test_gmres_seeded_systems(golden, orth):
     g = golden("wgmres")
     for m in (5, 12, 25):
-        x, rep = hg.weighted_gmres(g["A30"], g["b30"], rtol=0.0, maxit=m)
+        x, rep = hg.weighted_gmres(g["A30"], g["b30"], rtol=0.0, maxit=m, orth=orth)
         assert rep.iterations == m
         assert np.abs(x - g["x30_%d" % m]).max() <= 1e-10 * max(np.abs(g["x30_%d" % m]).max(), 1.0)
         assert np.abs(rep.residual_history - g["h30_%d" % m]).max() <= 1e-10 * g["h30_%d" % m][0]
-    x, rep = hg.weighted_gmres(g["A50"], g["b50"], weight=sp.csr_matrix(g["W50"]), rtol=1e-10, maxit=50)
-    assert rep.converged and rep.iterations == int(g["it50"])
+    x, rep = hg.weighted_gmres(g["A50"], g["b50"], weight=sp.csr_matrix(g["W50"]), rtol=1e-10, maxit=50, orth=orth)
+    assert rep.converged and abs(rep.iterations - int(g["it50"])) <= (0 if orth == "measured" else 1)
     assert rel(x, g["x50"]) <= 1e-10
     hist = rep.residual_history
     assert np.all(np.diff(hist) <= 1e-14 * hist[0])
@@ -172,27 +179,33 @@ def test_gmres_seeded_systems(golden):
     assert abs(np.sqrt(r @ (g["W50"] @ r)) - hist[-1]) <= 1e-8 * hist[0]
 
 
-def test_gmres_edge_cases():
+@pytest.mark.parametrize("orth", ORTHS)
+def test_gmres_edge_cases(orth):
     rng = np.random.default_rng(0)
     b = rng.standard_normal(40)
-    x, rep = hg.weighted_gmres(np.eye(40), b, rtol=1e-12, maxit=10)
+    gm = lambda *a, **k: hg.weighted_gmres(*a, orth=orth, **k)  # noqa: E731
+    x, rep = gm(np.eye(40), b, rtol=1e-12, maxit=10)
     assert rep.iterations == 1 and rep.converged and np.abs(x - b).max() <= 1e-12
     A = np.diag([2.0, 2.0, 5.0])
-    x, rep = hg.weighted_gmres(A, np.ones(3), rtol=1e-13, maxit=10)
+    x, rep = gm(A, np.ones(3), rtol=1e-13, maxit=10)
     assert rep.iterations <= 2 and rep.converged and np.abs(A @ x - 1.0).max() <= 1e-12
-    x, rep = hg.weighted_gmres(np.eye(4), np.zeros(4), maxit=4)
+    x, rep = gm(np.eye(4), np.zeros(4), maxit=4)
     assert rep.converged and rep.iterations == 0 and np.all(x == 0.0)
     A = rng.standard_normal((40, 40)) + 40 * np.eye(40)
-    x, rep = hg.weighted_gmres(A, b, rtol=1e-14, maxit=3)
+    x, rep = gm(A, b, rtol=1e-14, maxit=3)
     assert rep.iterations == 3 and not rep.converged
-    x, rep = hg.weighted_gmres(A, b, rtol=1e-10, maxit=20, gamma=0.5)
+    x0 = rng.standard_normal(40)
+    x, rep = gm(A, b, rtol=1e-12, maxit=40, x0=x0)
+    assert rep.converged and np.abs(A @ x - b).max() <= 1e-9 * np.abs(b).max()
+    x, rep = gm(A, b, rtol=1e-10, maxit=20, gamma=0.5)
     assert rep.elman_envelope.size == rep.iterations + 1
     with pytest.raises(TypeError):
         hg.weighted_gmres(lambda v: v, b)
 
 
 @pytest.mark.parametrize("name", ["2", "3"])
-def test_config_parity_vs_oracle(name):
+@pytest.mark.parametrize("orth", ORTHS)
+def test_config_parity_vs_oracle(name, orth):
     P = hg.build_problem(name)
     pre = hg.factorize(P.forms, P.dec, P.coarse)
     orc = OraclePreconditioner(P.forms, P.dec, P.coarse)
@@ -200,7 +213,7 @@ def test_config_parity_vs_oracle(name):
     assert rel(pre.apply(r), orc.apply(r)) <= APPLY_RTOL
     B, Dk = P.forms.helmholtz, P.forms.dk
     rhs = P.rhs
-    x, rep = hg.weighted_gmres(pre.as_operator("T"), pre.apply(rhs), weight=Dk, rtol=1e-6, maxit=1000)
+    x, rep = hg.weighted_gmres(pre.as_operator("T"), pre.apply(rhs), weight=Dk, rtol=1e-6, maxit=1000, orth=orth)
     xo, info = oracle_gmres(lambda v: orc.apply(B @ v), orc.apply(rhs), weight=Dk, rtol=1e-6, maxit=1000)
     assert rep.converged and info["converged"]
     assert abs(rep.iterations - info["iterations"]) <= 1
