@@ -155,6 +155,10 @@ const char* hg_last_error(void);
 /* Number of this library's kernels launched since load (counter). */
 int64_t hg_kernel_launches(void);
 int hg_device_sync(void);
+/* Process exit: later destroy calls return without touching the device
+ * (the CUDA driver may already be torn down when a host language's
+ * finalizers run; the Python binding registers this with atexit). */
+int hg_shutdown(void);
 
 /* ---- preconditioner (schwarz.factorize / TwoLevelPreconditioner) ---- */
 int hg_precond_create(const HgPrecondDesc* desc, HgPrecond** out);

@@ -5,6 +5,7 @@ see csrc/Makefile).  There is no fallback: if the library is missing or no
 CUDA device is present, the first call raises.
 """
 
+import atexit
 import ctypes
 import os
 
@@ -70,6 +71,7 @@ SIGNATURES = {
     "hg_last_error": (ctypes.c_char_p, []),
     "hg_kernel_launches": (ctypes.c_int64, []),
     "hg_device_sync": (ctypes.c_int, []),
+    "hg_shutdown": (ctypes.c_int, []),
     "hg_precond_create": (ctypes.c_int, [ctypes.POINTER(HgPrecondDesc), ctypes.POINTER(_vp)]),
     "hg_precond_destroy": (ctypes.c_int, [_vp]),
     "hg_precond_device_bytes": (ctypes.c_int64, [_vp]),
@@ -140,6 +142,7 @@ def load(path=LIB_PATH):
         raise ImportError("libhelmgpu.so ABI mismatch")
     if path == LIB_PATH:
         _LIB = lib
+        atexit.register(lib.hg_shutdown)
     return lib
 
 

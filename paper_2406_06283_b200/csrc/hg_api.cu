@@ -75,6 +75,7 @@ struct Workspace {
 struct VmBuf {
   CUdeviceptr base = 0;
   size_t reserved = 0, mapped = 0, gran = 0;
+  bool plain = false;  // HG_VMM=0: one cudaMalloc of the whole reservation (tools without VMM support)
   std::vector<CUmemGenericAllocationHandle> handles;
   std::vector<size_t> sizes;
   int dev = 0;
@@ -128,6 +129,15 @@ static CUmemAllocationProp vm_prop(int dev) {
 
 int VmBuf::reserve(size_t bytes) {
   free_all();
+  static const bool no_vmm = getenv("HG_VMM") && getenv("HG_VMM")[0] == '0';
+  if (no_vmm) {
+    void* p = nullptr;
+    HG_CUDA_TRY(cudaMalloc(&p, bytes));
+    base = reinterpret_cast<CUdeviceptr>(p);
+    reserved = mapped = bytes;
+    plain = true;
+    return HG_OK;
+  }
   const DrvApi& d = drv();
   if (!d.ok) {
     set_error("CUDA virtual memory management entry points unavailable");
@@ -188,8 +198,21 @@ int VmBuf::ensure(size_t bytes) {
   return HG_OK;
 }
 
+static bool g_shutdown = false;  // hg_shutdown: the process is exiting, skip device frees
+
 void VmBuf::free_all() {
   if (!base) return;
+  if (g_shutdown) {  // the driver may already be torn down at interpreter exit: leak, the process ends
+    base = 0;
+    return;
+  }
+  if (plain) {
+    cudaFree(reinterpret_cast<void*>(base));
+    base = 0;
+    reserved = mapped = 0;
+    plain = false;
+    return;
+  }
   const DrvApi& d = drv();
   cudaDeviceSynchronize();
   size_t off = 0;
@@ -547,8 +570,13 @@ int hg_device_sync(void) {
   return HG_OK;
 }
 
+int hg_shutdown(void) {
+  g_shutdown = true;
+  return HG_OK;
+}
+
 int hg_precond_destroy(HgPrecond* P) {
-  if (!P) return HG_OK;
+  if (!P || g_shutdown) return HG_OK;
   release(P->A.indptr);
   release(P->A.indices);
   release(P->A.data);
@@ -971,7 +999,7 @@ int hg_op_create_precond(HgPrecond* P, int mode, HgOp** out) {
 }
 
 int hg_op_destroy(HgOp* op) {
-  if (!op) return HG_OK;
+  if (!op || g_shutdown) return HG_OK;
   if (op->kind == 0) {
     release(op->csr.indptr);
     release(op->csr.indices);

@@ -43,21 +43,29 @@ constexpr int LS_CH = 16;  // steps per staged chunk
 constexpr int LS_NS = 6;   // ring stages
 constexpr int LS_THREADS = 64;        // single right-hand side: 1 consumer + 1 producer warp
 
+// Every sweep function is templated on K, the right-hand sides one consumer
+// warp carries: each staged multiplier is loaded from shared memory once and
+// applied to K windows (K = 1: the single-RHS chain; K = LS_KM: the batched
+// kernel, where shared-memory bandwidth and not the chain bounds the step).
+
 // Row interchange of rows j (register 0, lane s) and l (register (l-j0)/32,
 // lane (l-j0)%32) in the distributed window; warp-uniform, ~0.2% of steps.
-template <int R>
-__device__ __forceinline__ void ls_swap(double (&v)[R], int s, int l, int j0, int lane) {
+template <int K, int R>
+__device__ __forceinline__ void ls_swap(double (&v)[K][R], int s, int l, int j0, int lane) {
   const int rl = (l - j0) >> 5, ll = (l - j0) & 31;
-  const double a = __shfl_sync(FULL, v[0], s);
-  double sel = v[0];
 #pragma unroll
-  for (int r = 1; r < R; ++r)
-    if (r == rl) sel = v[r];
-  const double b = __shfl_sync(FULL, sel, ll);
+  for (int k = 0; k < K; ++k) {
+    const double a = __shfl_sync(FULL, v[k][0], s);
+    double sel = v[k][0];
 #pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (r == rl && lane == ll) v[r] = a;
-  if (lane == s) v[0] = b;
+    for (int r = 1; r < R; ++r)
+      if (r == rl) sel = v[k][r];
+    const double b = __shfl_sync(FULL, sel, ll);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (r == rl && lane == ll) v[k][r] = a;
+    if (lane == s) v[k][0] = b;
+  }
 }
 
 template <int R>
@@ -79,84 +87,109 @@ struct SweepCtx {
 // pivot (FWD) or 1/u_jj (BWD).  lim = kw - lane.  Multipliers outside the
 // band are skipped by predication (only registers 0, R-2, R-1 can be partly
 // outside: R = 1 + ceil(kw/32) keeps registers 1..R-3 inside).
-template <int R, bool FWD, int S>
-__device__ __forceinline__ void ls_step(double (&v)[R], double (&f)[4], const double* __restrict__ rec, int lane,
-                                        int lim, int kw) {
+template <int K, int R, bool FWD, int S>
+__device__ __forceinline__ void ls_step(double (&v)[K][R], double (&f)[K][4], const double* __restrict__ rec,
+                                        int lane, int lim, int kw) {
   constexpr int p = S & 3;
-  double bj = f[p];
+  double bj[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) bj[k] = f[k][p];
   if (!FWD) {
-    bj = f[p] * rec[kw];
-    if (lane == S) v[0] = bj;
+    const double dinv = rec[kw];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      bj[k] = f[k][p] * dinv;
+      if (lane == S) v[k][0] = bj[k];
+    }
   }
   const double2 m01 = *reinterpret_cast<const double2*>(rec);  // 16-byte aligned: even stride
   const double m2 = rec[2];
   // front (every lane): the critical chain is f[p+1] -> next step's pivot
-  f[(p + 1) & 3] = fma(-m01.x, bj, f[(p + 1) & 3]);
-  f[(p + 2) & 3] = fma(-m01.y, bj, f[(p + 2) & 3]);
-  f[(p + 3) & 3] = fma(-m2, bj, f[(p + 3) & 3]);
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    f[k][(p + 1) & 3] = fma(-m01.x, bj[k], f[k][(p + 1) & 3]);
+    f[k][(p + 2) & 3] = fma(-m01.y, bj[k], f[k][(p + 2) & 3]);
+    f[k][(p + 3) & 3] = fma(-m2, bj[k], f[k][(p + 3) & 3]);
+  }
   // distributed window
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int t = 32 * r + lane - S;
     const bool edge = (r == 0) || (r >= R - 2);
     const bool on = !edge || ((r == 0 ? (lane > S) : true) && (32 * r - S <= lim));
-    if (on) v[r] = fma(-rec[t - 1], bj, v[r]);
+    if (on) {
+      const double m = rec[t - 1];
+#pragma unroll
+      for (int k = 0; k < K; ++k) v[k][r] = fma(-m, bj[k], v[k][r]);
+    }
   }
-  f[p] = ls_fetch<R>(v, S + 4);  // row j+4, includes this step's update
+#pragma unroll
+  for (int k = 0; k < K; ++k) f[k][p] = ls_fetch<R>(v[k], S + 4);  // row j+4, includes this step's update
 }
 
 // Straight-line round of 32 steps without pivots (the common case).
-template <int R, bool FWD, int S>
-__device__ __forceinline__ void ls_round_fast(double (&v)[R], double (&f)[4], const double* rec0,
+template <int K, int R, bool FWD, int S>
+__device__ __forceinline__ void ls_round_fast(double (&v)[K][R], double (&f)[K][4], const double* rec0,
                                               const double* rec1, int stride, int lane, int lim, int kw) {
   if constexpr (S < 32) {
-    ls_step<R, FWD, S>(v, f, (S < LS_CH ? rec0 : rec1) + S * stride, lane, lim, kw);
-    ls_round_fast<R, FWD, S + 1>(v, f, rec0, rec1, stride, lane, lim, kw);
+    ls_step<K, R, FWD, S>(v, f, (S < LS_CH ? rec0 : rec1) + S * stride, lane, lim, kw);
+    ls_round_fast<K, R, FWD, S + 1>(v, f, rec0, rec1, stride, lane, lim, kw);
   }
 }
 
 // General round: partial (last) round and/or row interchanges.
-template <int R, bool FWD, int S>
-__device__ __forceinline__ void ls_round_slow(double (&v)[R], double (&f)[4], const double* rec0,
+template <int K, int R, bool FWD, int S>
+__device__ __forceinline__ void ls_round_slow(double (&v)[K][R], double (&f)[K][4], const double* rec0,
                                               const double* rec1, int stride, int lane, int lim, int kw,
                                               unsigned swapmask, int pl, int j0, int nsteps) {
   if constexpr (S < 32) {
     if (S < nsteps) {
       if (FWD && ((swapmask >> S) & 1u)) {
         // row interchange: permute the distributed window, refresh the front
-        ls_swap<R>(v, S, __shfl_sync(FULL, pl, S), j0, lane);
-        f[S & 3] = ls_fetch<R>(v, S);
-        f[(S + 1) & 3] = ls_fetch<R>(v, S + 1);
-        f[(S + 2) & 3] = ls_fetch<R>(v, S + 2);
-        f[(S + 3) & 3] = ls_fetch<R>(v, S + 3);
+        ls_swap<K, R>(v, S, __shfl_sync(FULL, pl, S), j0, lane);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          f[k][S & 3] = ls_fetch<R>(v[k], S);
+          f[k][(S + 1) & 3] = ls_fetch<R>(v[k], S + 1);
+          f[k][(S + 2) & 3] = ls_fetch<R>(v[k], S + 2);
+          f[k][(S + 3) & 3] = ls_fetch<R>(v[k], S + 3);
+        }
       }
-      ls_step<R, FWD, S>(v, f, (S < LS_CH ? rec0 : rec1) + S * stride, lane, lim, kw);
-      ls_round_slow<R, FWD, S + 1>(v, f, rec0, rec1, stride, lane, lim, kw, swapmask, pl, j0, nsteps);
+      ls_step<K, R, FWD, S>(v, f, (S < LS_CH ? rec0 : rec1) + S * stride, lane, lim, kw);
+      ls_round_slow<K, R, FWD, S + 1>(v, f, rec0, rec1, stride, lane, lim, kw, swapmask, pl, j0, nsteps);
     }
   }
 }
 
-// One sweep over n rows. FWD: input gathered from r[idx[row]], output y[row]
-// into xs. !FWD: input y from xs in reverse, output x into xs in reverse.
-template <int R, bool FWD>
+// One sweep over n rows for kc <= K right-hand sides (column k: input
+// rin + k * ldr, scratch xs + k * xs_len).  FWD: input gathered from
+// r[idx[row]], output y[row] into xs.  !FWD: input y from xs in reverse,
+// output x into xs in reverse.
+template <int K, int R, bool FWD>
 __device__ void ls_sweep(const SweepCtx& cx, int& chunk, int n, int kw, int stride,
-                         const int* __restrict__ idx, const double* __restrict__ rin,
-                         double* __restrict__ xs, int dbg) {
+                         const int* __restrict__ idx, const double* __restrict__ rin, long long ldr,
+                         double* __restrict__ xs, long long xs_len, int kc, int dbg) {
   static_assert(R >= 2, "window must hold row j+4 of every step");
   const int lane = threadIdx.x & 31;
-  auto load_in = [&](int row) -> double {
-    if (row >= n) return 0.0;
-    if (FWD) return __ldg(rin + __ldg(idx + row));
-    return xs[n - 1 - row];
+  auto load_in = [&](int k, int row) -> double {
+    if (row >= n || k >= kc) return 0.0;
+    if (FWD) return __ldg(rin + (long long)k * ldr + __ldg(idx + row));
+    return xs[(long long)k * xs_len + n - 1 - row];
   };
   const int lim = kw - lane;
-  double v[R];
+  double v[K][R], f[K][4], pre[K];
 #pragma unroll
-  for (int r = 0; r < R; ++r) v[r] = load_in(32 * r + lane);
-  double pre = load_in(32 * R + lane);
-  double f[4] = {ls_fetch<R>(v, 0), ls_fetch<R>(v, 1), ls_fetch<R>(v, 2), ls_fetch<R>(v, 3)};
+  for (int k = 0; k < K; ++k) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[k][r] = load_in(k, 32 * r + lane);
+    pre[k] = load_in(k, 32 * R + lane);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) f[k][q] = ls_fetch<R>(v[k], q);
+  }
   for (int j0 = 0; j0 < n; j0 += 32) {
-    const double nxt = load_in(j0 + 32 * R + 32 + lane);
+    double nxt[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) nxt[k] = load_in(k, j0 + 32 * R + 32 + lane);
     // the round's records: one or two staged chunks
     const int nch = (min(32, n - j0) + LS_CH - 1) / LS_CH;
     const int st0 = chunk % LS_NS;
@@ -181,9 +214,9 @@ __device__ void ls_sweep(const SweepCtx& cx, int& chunk, int n, int kw, int stri
     if (!(dbg & 2)) {
       const int nsteps = min(32, n - j0);
       if (nsteps == 32 && swapmask == 0u)
-        ls_round_fast<R, FWD, 0>(v, f, rec0, rec1, stride, lane, lim, kw);
+        ls_round_fast<K, R, FWD, 0>(v, f, rec0, rec1, stride, lane, lim, kw);
       else
-        ls_round_slow<R, FWD, 0>(v, f, rec0, rec1, stride, lane, lim, kw, swapmask, pl, j0, nsteps);
+        ls_round_slow<K, R, FWD, 0>(v, f, rec0, rec1, stride, lane, lim, kw, swapmask, pl, j0, nsteps);
     }
     __syncwarp();
     if (lane == 0) {
@@ -192,37 +225,42 @@ __device__ void ls_sweep(const SweepCtx& cx, int& chunk, int n, int kw, int stri
     }
     chunk += nch;
     const int row = j0 + lane;
-    if (row < n) {
-      if (FWD)
-        xs[row] = v[0];
-      else
-        xs[n - 1 - row] = v[0];
-    }
 #pragma unroll
-    for (int r = 0; r + 1 < R; ++r) v[r] = v[r + 1];
-    v[R - 1] = pre;
-    pre = nxt;
+    for (int k = 0; k < K; ++k) {
+      if (row < n && k < kc) {
+        if (FWD)
+          xs[(long long)k * xs_len + row] = v[k][0];
+        else
+          xs[(long long)k * xs_len + n - 1 - row] = v[k][0];
+      }
+#pragma unroll
+      for (int r = 0; r + 1 < R; ++r) v[k][r] = v[k][r + 1];
+      v[k][R - 1] = pre[k];
+      pre[k] = nxt[k];
+    }
   }
 }
 
-// Multi-RHS (nw > 1 consumer warps): consumer warp w solves right-hand side
-// column w (input r + w * ldr, output xs + w * xs_len) against the SAME staged
-// factor records, so the factors stream from HBM once for all columns; every
-// consumer warp releases each ring stage (empty barrier count = nw).
-// The body is shared by two kernels with different launch bounds: the
-// single-RHS kernel (64 threads, hg_local.cu) keeps the register schedule of
-// a one-warp chain; the multi-RHS kernel (HG_MAX_RHS + 1 warps,
-// hg_local_multi.cu) is bounded to one 544-thread block per SM.
-template <int RF, int RB, bool MULTI>
+constexpr int LS_KM = 2;  // right-hand sides per consumer warp in the batched kernel (4 spills past 255 registers)
+
+// K right-hand sides per consumer warp; consumer warp w solves columns
+// w*K .. min(w*K + K, nrhs) - 1 (input r + c * ldr, output xs + c * xs_len)
+// against the SAME staged factor records, so the factors stream from HBM
+// once for all columns; every consumer warp releases each ring stage (empty
+// barrier count = consumer warps).  Two kernels share the body with their
+// own launch bounds: the single-RHS chain (64 threads, hg_local.cu) and the
+// batched one (HG_MAX_RHS / LS_KM + 1 warps, hg_local_multi.cu).
+template <int RF, int RB, int K>
 __device__ __forceinline__ void local_solve_body(const LocalDesc* __restrict__ descs, const int* __restrict__ idx,
                                                  const double* __restrict__ fwd, const double* __restrict__ bwd,
                                                  const double* __restrict__ r, double* __restrict__ xs,
-                                                 int stage_stride, int dbg, long long ldr, long long xs_len) {
-extern __shared__ __align__(128) double ring[];
+                                                 int stage_stride, int dbg, long long ldr, long long xs_len,
+                                                 int nrhs) {
+  extern __shared__ __align__(128) double ring[];
   __shared__ __align__(8) uint64_t full[LS_NS], empty[LS_NS];
   const LocalDesc d = descs[blockIdx.x];
-  const int nw = MULTI ? (int)(blockDim.x >> 5) - 1 : 1;  // consumer warps = right-hand sides
-  const int warp = MULTI ? (int)(threadIdx.x >> 5) : (threadIdx.x >= 32 ? 1 : 0);
+  const int nw = K == 1 ? 1 : (int)(blockDim.x >> 5) - 1;  // consumer warps
+  const int warp = K == 1 ? (threadIdx.x >= 32 ? 1 : 0) : (int)(threadIdx.x >> 5);
   if (threadIdx.x == 0) {
     for (int s = 0; s < LS_NS; ++s) {
       mbar_init(&full[s], 1);
@@ -252,13 +290,15 @@ extern __shared__ __align__(128) double ring[];
   }
   SweepCtx cx{ring, full, empty, stage_stride};
   int chunk = 0;
-  double* xsb = MULTI ? xs + (long long)warp * xs_len + d.idx_off : xs + d.idx_off;
-  const double* rin = MULTI ? r + (long long)warp * ldr : r;
+  const int c0 = K == 1 ? 0 : warp * K;
+  const int kc = K == 1 ? 1 : min(K, nrhs - c0);
+  double* xsb = xs + (long long)c0 * xs_len + d.idx_off;
+  const double* rin = r + (long long)c0 * ldr;
   const long long t0 = clock64();
-  ls_sweep<RF, true>(cx, chunk, d.n, d.kl, d.fstride, idx + d.idx_off, rin, xsb, dbg);
+  ls_sweep<K, RF, true>(cx, chunk, d.n, d.kl, d.fstride, idx + d.idx_off, rin, ldr, xsb, xs_len, kc, dbg);
   __syncwarp();
   const long long t1 = clock64();
-  ls_sweep<RB, false>(cx, chunk, d.n, d.kv, d.bstride, nullptr, nullptr, xsb, dbg);
+  ls_sweep<K, RB, false>(cx, chunk, d.n, d.kv, d.bstride, nullptr, nullptr, 0, xsb, xs_len, kc, dbg);
   if ((dbg & 4) && blockIdx.x < 2 && threadIdx.x == 0) {
     const long long t2 = clock64();
     printf("block %d n=%d kl=%d kv=%d: fwd %.1f cyc/step, bwd %.1f cyc/step\n", blockIdx.x, d.n, d.kl, d.kv,
@@ -273,20 +313,20 @@ __global__ void __launch_bounds__(LS_THREADS) k_local_solve(const LocalDesc* __r
                                                            const double* __restrict__ bwd,
                                                            const double* __restrict__ r, double* __restrict__ xs,
                                                            int stage_stride, int dbg, long long ldr,
-                                                           long long xs_len) {
-  local_solve_body<RF, RB, false>(descs, idx, fwd, bwd, r, xs, stage_stride, dbg, ldr, xs_len);
+                                                           long long xs_len, int nrhs) {
+  local_solve_body<RF, RB, 1>(descs, idx, fwd, bwd, r, xs, stage_stride, dbg, ldr, xs_len, nrhs);
 }
 
 template <int RF, int RB>
-__global__ void __launch_bounds__(32 * (HG_MAX_RHS + 1), 1) k_local_solve_multi(
+__global__ void __launch_bounds__(32 * (HG_MAX_RHS / LS_KM + 1), 2) k_local_solve_multi(
     const LocalDesc* __restrict__ descs, const int* __restrict__ idx, const double* __restrict__ fwd,
     const double* __restrict__ bwd, const double* __restrict__ r, double* __restrict__ xs, int stage_stride, int dbg,
-    long long ldr, long long xs_len) {
-  local_solve_body<RF, RB, true>(descs, idx, fwd, bwd, r, xs, stage_stride, dbg, ldr, xs_len);
+    long long ldr, long long xs_len, int nrhs) {
+  local_solve_body<RF, RB, LS_KM>(descs, idx, fwd, bwd, r, xs, stage_stride, dbg, ldr, xs_len, nrhs);
 }
 
 using LocalKernel = void (*)(const LocalDesc*, const int*, const double*, const double*, const double*,
-                             double*, int, int, long long, long long);
+                             double*, int, int, long long, long long, int);
 
 template <int RF, int RB, int NW>
 static LocalKernel pick2() {
@@ -343,8 +383,9 @@ static int launch_local_grid_t(HgPrecond* P, const LocalDesc* descs, int nblocks
     configured[P->rf][P->rb] = smem;
   }
   static const int dbg = getenv("HG_LOCAL_DEBUG") ? atoi(getenv("HG_LOCAL_DEBUG")) : 0;  // timing experiments only
-  k<<<nblocks, 32 * (nrhs + 1), smem, st>>>(descs, P->d_local_idx, P->d_fwd, P->d_bwd, r, xs ? xs : P->d_xs,
-                                             stage_stride, dbg, ldr, xs_len);
+  const int nwarps = NW == 1 ? 1 : (nrhs + LS_KM - 1) / LS_KM;  // consumer warps
+  k<<<nblocks, 32 * (nwarps + 1), smem, st>>>(descs, P->d_local_idx, P->d_fwd, P->d_bwd, r, xs ? xs : P->d_xs,
+                                               stage_stride, dbg, ldr, xs_len, nrhs);
   HG_LAUNCH_CHECK();
   return HG_OK;
 }

@@ -14,7 +14,8 @@
 //  k_b0_multi    Y = B0^{-1} C with the tiled getrf factors (hg_b0.cu /
 //                hg_b0c.cu layout): persistent CTAs, panel t owned by CTA
 //                t % G, each 64 x 64 x 16 tile product on DMMA, panels
-//                published through a monotone L2 counter (release/acquire).
+//                handed over as (value, tag) pairs in L2 (the data is the
+//                flag: one round trip per hop).
 //  k_zy_multi    U_b = Z_b Y_b (256 rows x m_b x 16) on DMMA.
 //  k_assemble_multi  out = coarse + local contributions in the reference's
 //                fixed summation order (schwarz.py:52-61), per column.
@@ -277,65 +278,89 @@ struct B0MultiArgs {
   const long long* tile_ptr;
   const int* tile_col;
   const double* tiles;      // [ntile][64][64]
-  double* xbuf;             // [2][K*64][MR]
+  double* xbuf;             // [2K][64][MR] (value, tag) pairs: 2 doubles each
   double* y;                // [m][MR]
-  unsigned long long* done;
-  unsigned long long base;
+  double tag0;              // tag of panel g in this launch: tag0 + g (unique across launches)
   const unsigned long long* zt_done;
   unsigned long long zt_target;
 };
+
+// 16-byte (value, tag) pair access: written and read as one vector access,
+// L1 bypassed on the read side.
+__device__ __forceinline__ void st_pair(double* p, double v, double tag) {
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v), "d"(tag) : "memory");
+}
+__device__ __forceinline__ double2 ld_pair(const double* p) {
+  double2 r;
+  asm volatile("ld.volatile.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p) : "memory");
+  return r;
+}
+
+// Load panel gp (64 x MR values) of this launch into s_x, spinning until every
+// pair carries the panel's tag: the data is its own completion flag, so a hop
+// costs one L2 round trip (no counter, no fence, no ordered publication).
+__device__ __forceinline__ void wait_panel(const double* __restrict__ xbuf, int gp, double tag, double* s_x,
+                                           bool reversed, int K) {
+  // thread t covers pairs t, t + 256, t + 512, t + 768 of the panel (rows r = e / MR)
+  const double* base = xbuf + (size_t)gp * BP * MR * 2;
+  double v[4];
+  bool ok;
+  do {
+    ok = true;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = threadIdx.x + 256 * q;
+      const double2 p = ld_pair(base + 2 * e);
+      v[q] = p.x;
+      ok = ok && (p.y == tag);
+    }
+  } while (!ok);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int e = threadIdx.x + 256 * q;
+    const int r = e / MR, c = e % MR;
+    s_x[(reversed ? BP - 1 - r : r) * SR + c] = v[q];
+  }
+  (void)K;
+}
 
 // Panel g (phase ph = g / K: 0 = L solve of P c, 1 = U solve in reversed
 // coordinates of the L solution) of 64 rows x nrhs columns; warp w owns
 // panel rows 8w..8w+7.  premul (cluster layout): tiles are D_t^{-1} T[t, j]
 // and x_t = D_t^{-1} rhs_t - sum_j M[t, j] x_j; otherwise
 // x_t = D_t^{-1} (rhs_t - sum_j T[t, j] x_j).  Tiles in ascending j: the
-// summation order is fixed, the result deterministic.
+// summation order is fixed, the result deterministic.  Panels are handed
+// over as tagged pairs in global memory (wait_panel).
 __global__ void __launch_bounds__(256, 1) k_b0_multi(B0MultiArgs a) {
   __shared__ __align__(16) double s_x[BP * SR];
-  __shared__ unsigned long long s_seen;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = lane & 3, g8 = lane >> 2;
   const int row = warp * 8 + g8;
   const int K = a.K;
-  auto observe = [&](unsigned long long need) -> unsigned long long {
-    if (tid == 0) {
-      unsigned long long v = ld_acq(a.done);
-      while (v < need) v = ld_acq(a.done);
-      s_seen = v;
-    }
-    __syncthreads();
-    return s_seen;
-  };
   if (tid == 0)
     while (ld_acq(a.zt_done) < a.zt_target) {
     }
   __syncthreads();
-  unsigned long long seen = 0;
   for (int g = blockIdx.x; g < 2 * K; g += gridDim.x) {
     const int ph = g / K, t = g % K;
-    const unsigned long long pbase = a.base + (unsigned long long)ph * K;
     const double* dinv_g = a.dinv + (size_t)g * BTILE;
     double av[16];
     if (a.premul) load_afrag(av, dinv_g, row, q, a.swz, 1.0);
-    if (ph == 1 && seen < a.base + K) seen = observe(a.base + K);  // the whole L solve
     __syncthreads();  // s_x free
-    for (int e = tid; e < BP * MR; e += 256) {
-      const int r = e / MR, c = e % MR;
-      double v = 0.0;
-      if (c < a.nrhs) {
-        if (ph == 0) {
-          const int i = t * BP + r;
-          if (i < a.m) {
-            const int col = a.perm[i];
-            const CblkDesc d = a.descs[a.col_blk[col]];
-            const int l = col - d.col0;
-            for (int ch = 0; ch < d.nchunk; ++ch) v += a.cpartm[(d.part_off + (long long)ch * d.m + l) * MR + c];
-          }
-        } else {
-          v = a.xbuf[((size_t)K * BP - 1 - (t * BP + r)) * MR + c];
+    if (ph == 0) {
+      for (int e = tid; e < BP * MR; e += 256) {
+        const int r = e / MR, c = e % MR;
+        double v = 0.0;
+        const int i = t * BP + r;
+        if (c < a.nrhs && i < a.m) {
+          const int col = a.perm[i];
+          const CblkDesc d = a.descs[a.col_blk[col]];
+          const int l = col - d.col0;
+          for (int ch = 0; ch < d.nchunk; ++ch) v += a.cpartm[(d.part_off + (long long)ch * d.m + l) * MR + c];
         }
+        s_x[r * SR + c] = v;
       }
-      s_x[r * SR + c] = v;
+    } else {  // the reversed L solution of panel K-1-t
+      wait_panel(a.xbuf, K - 1 - t, a.tag0 + (K - 1 - t), s_x, true, K);
     }
     __syncthreads();
     double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
@@ -349,18 +374,10 @@ __global__ void __launch_bounds__(256, 1) k_b0_multi(B0MultiArgs a) {
     }
     const long long e0 = a.tile_ptr[g], e1 = a.tile_ptr[g + 1];
     for (long long e = e0; e < e1; ++e) {
-      const int j = a.tile_col[e];
+      const int gj = ph * K + a.tile_col[e];
       load_afrag(av, a.tiles + (size_t)e * BTILE, row, q, a.swz, -1.0);  // in flight across the wait
-      if (seen < pbase + j + 1) seen = observe(pbase + j + 1);
       __syncthreads();  // s_x free
-      {
-        const double2* src = reinterpret_cast<const double2*>(a.xbuf + ((size_t)(ph * K + j) * BP) * MR);
-        for (int e2 = tid; e2 < BP * MR / 2; e2 += 256) {
-          const double2 v = src[e2];
-          const int r = (2 * e2) / MR, c = (2 * e2) % MR;
-          *reinterpret_cast<double2*>(s_x + r * SR + c) = v;
-        }
-      }
+      wait_panel(a.xbuf, gj, a.tag0 + gj, s_x, false, K);
       __syncthreads();
       mma_tile(acc, av, s_x, q, g8);
     }
@@ -373,9 +390,13 @@ __global__ void __launch_bounds__(256, 1) k_b0_multi(B0MultiArgs a) {
       acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.0;
       mma_tile(acc, av, s_x, q, g8);
     }
-    double* xo = a.xbuf + ((size_t)(ph * K + t) * BP + row) * MR;
-    *reinterpret_cast<double2*>(xo + 2 * q) = make_double2(acc[0][0], acc[0][1]);
-    *reinterpret_cast<double2*>(xo + 8 + 2 * q) = make_double2(acc[1][0], acc[1][1]);
+    // publish: every value with the panel's tag (no fence: each pair is its own flag)
+    const double tag = a.tag0 + g;
+    double* xo = a.xbuf + ((size_t)g * BP + row) * MR * 2;
+    st_pair(xo + 2 * (2 * q), acc[0][0], tag);
+    st_pair(xo + 2 * (2 * q + 1), acc[0][1], tag);
+    st_pair(xo + 2 * (8 + 2 * q), acc[1][0], tag);
+    st_pair(xo + 2 * (8 + 2 * q + 1), acc[1][1], tag);
     if (ph == 1) {
       const int i = K * BP - 1 - (t * BP + row);
       if (i < a.m) {
@@ -383,13 +404,6 @@ __global__ void __launch_bounds__(256, 1) k_b0_multi(B0MultiArgs a) {
         *reinterpret_cast<double2*>(yo + 2 * q) = make_double2(acc[0][0], acc[0][1]);
         *reinterpret_cast<double2*>(yo + 8 + 2 * q) = make_double2(acc[1][0], acc[1][1]);
       }
-    }
-    __syncthreads();
-    if (tid == 0) {  // publish in panel order (release covers the CTA's stores ordered by the barrier)
-      __threadfence();
-      while (ld_acq(a.done) < a.base + g) {
-      }
-      st_rel(a.done, a.base + g + 1);
     }
   }
 }
@@ -403,9 +417,10 @@ int launch_b0_multi(HgPrecond* P, int nrhs, cudaStream_t st, unsigned long long 
   const int K = P->b0_K;
   static const int env_g = getenv("HG_B0M_CTAS") ? atoi(getenv("HG_B0M_CTAS")) : 0;
   const int G = std::min(K, env_g > 0 ? env_g : 16);
+  // tags stay below 2^53 (exact in a double) for ~10^12 launches
   B0MultiArgs a{P->m, K, nrhs, P->b0_mode == 1 ? 1 : 0, P->b0_mode == 1 ? 1 : 0, P->d_b0_perm, P->d_col_blk,
                 P->d_cblk, P->d_cpartm, P->d_b0_dinv, P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles,
-                P->d_b0m_x, P->d_ym, P->d_b0m_done, P->b0m_epoch, P->d_zt_done, zt_target};
+                P->d_b0m_x, P->d_ym, (double)(P->b0m_epoch + 1), P->d_zt_done, zt_target};
   P->b0m_epoch += 2ull * K;
   k_b0_multi<<<G, 256, 0, st>>>(a);
   HG_LAUNCH_CHECK();
@@ -593,7 +608,8 @@ int multi_prepare(HgPrecond* P) {
     HG_TRY(alloc(&P->d_zsm, (size_t)MR * P->zs_len));
     HG_TRY(alloc(&P->d_cpartm, (size_t)MR * P->part_len));
     HG_TRY(alloc(&P->d_ym, (size_t)MR * P->m));
-    HG_TRY(alloc(&P->d_b0m_x, (size_t)2 * P->b0_K * BP * MR));
+    HG_TRY(alloc(&P->d_b0m_x, (size_t)2 * P->b0_K * BP * MR * 2));  // (value, tag) pairs
+    HG_CUDA_TRY(cudaMemset(P->d_b0m_x, 0, sizeof(double) * 2 * P->b0_K * BP * MR * 2));  // tag 0 = never
     HG_CUDA_TRY(cudaMalloc(&P->d_b0m_done, sizeof(unsigned long long)));
     HG_CUDA_TRY(cudaMemset(P->d_b0m_done, 0, sizeof(unsigned long long)));
     P->b0m_epoch = 0;
