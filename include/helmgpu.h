@@ -92,7 +92,10 @@ typedef struct {
    *   backward record r (r = 0..n_s-1, j = n_s-1-r):
    *                                      [u_{j-1,j}, ..., u_{j-kv,j}, 1/u_jj, pad]
    * with local_fstride / local_bstride doubles per record (even), zeros past
-   * the end of the block, ipiv stored as an exact double (0-based). */
+   * the end of the block, ipiv stored as an exact double (0-based).  With
+ * R_f = max(2, 1 + ceil(max_s kl_s / 32)) (R_b likewise from kv), every
+ * non-empty block needs kl_s >= 32 R_f - 65 and kv_s >= 32 R_b - 65: pad
+ * narrower blocks with zero multipliers (hg_precond_create checks). */
   int32_t n_local;
   const int32_t* local_n;
   const int32_t* local_kl;

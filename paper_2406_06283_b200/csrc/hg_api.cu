@@ -686,6 +686,17 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
   }
   P->rf = std::max(2, 1 + (max_kl + 31) / 32);
   P->rb = std::max(2, 1 + (max_kv + 31) / 32);
+  // registers 1..R-3 of the sweep window are applied without a band test:
+  // every block's records must cover them (factor.record_floor pads)
+  for (int s = 0; s < D->n_local; ++s) {
+    const LocalDesc& d = P->h_local[s];
+    if (d.n > 0 && (d.kl < 32 * P->rf - 65 || d.kv < 32 * P->rb - 65)) {
+      set_error("hg_precond_create: block " + std::to_string(s) + " records narrower than the launch's floor (kl " +
+                std::to_string(d.kl) + " < " + std::to_string(32 * P->rf - 65) + " or kv " + std::to_string(d.kv) +
+                " < " + std::to_string(32 * P->rb - 65) + "); zero pad them (factor.record_floor)");
+      return HG_ERR_ARG;
+    }
+  }
   if (D->n_local > 0 && (P->rf > 6 || P->rb > 10)) {
     set_error("hg_precond_create: local bandwidth kl=" + std::to_string(max_kl) + ", kv=" +
               std::to_string(max_kv) + " beyond compiled tiles (kl <= 160, kv <= 288)");

@@ -86,7 +86,8 @@ struct SweepCtx {
 // Record layout: rec[t-1] = multiplier of row j+t (t = 1..kw), rec[kw] =
 // pivot (FWD) or 1/u_jj (BWD).  lim = kw - lane.  Multipliers outside the
 // band are skipped by predication (only registers 0, R-2, R-1 can be partly
-// outside: R = 1 + ceil(kw/32) keeps registers 1..R-3 inside).
+// outside: R = 1 + ceil(kw_max/32) and every block's records padded to
+// kw >= 32 R - 65 keep registers 1..R-3 inside; hg_precond_create checks).
 template <int K, int R, bool FWD, int S>
 __device__ __forceinline__ void ls_step(double (&v)[K][R], double (&f)[K][4], const double* __restrict__ rec,
                                         int lane, int lim, int kw) {

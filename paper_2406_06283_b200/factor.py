@@ -112,11 +112,27 @@ def _even(x):
 MIN_RECORD_WIDTH = 3  # the kernel's replicated front reads the first 3 multipliers
 
 
-def pack_band_records(f):
+def register_tiles(kw):
+    """Register tiles (rows / 32) the device sweep compiles for a bandwidth:
+    R = max(2, 1 + ceil(kw / 32)) (hg_api.cu precond_create)."""
+    return max(2, 1 + (kw + 31) // 32)
+
+
+def record_floor(kw_max):
+    """Smallest record width a block may have in a launch whose widest block
+    has bandwidth kw_max.  The sweep applies registers 1..R-3 of the window
+    without a band test; that is exact only if every block's band covers
+    them, i.e. kw >= 32 R - 65.  Narrower blocks are zero padded to it (zero
+    multipliers leave the window unchanged)."""
+    return max(0, 32 * register_tiles(kw_max) - 65)
+
+
+def pack_band_records(f, kl_floor=0, kv_floor=0):
     """(fwd records, bwd records, fstride, bstride, kl_rec, kv_rec) for one
-    BandLU; widths below MIN_RECORD_WIDTH are zero padded (kl_rec, kv_rec)."""
+    BandLU; widths below MIN_RECORD_WIDTH or the launch's record floors
+    (record_floor) are zero padded (kl_rec, kv_rec)."""
     n, kl, kv = f.n, f.kl, f.kv
-    klp, kvp = max(kl, MIN_RECORD_WIDTH), max(kv, MIN_RECORD_WIDTH)
+    klp, kvp = max(kl, MIN_RECORD_WIDTH, kl_floor), max(kv, MIN_RECORD_WIDTH, kv_floor)
     fs, bs = _even(klp + 1), _even(kvp + 1)
     fwd = np.zeros((n, fs))
     bwd = np.zeros((n, bs))

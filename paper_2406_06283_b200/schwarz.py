@@ -24,7 +24,8 @@ import scipy.sparse as sp
 
 from . import _lib
 from .errors import SingularOperatorError
-from .factor import band_lu, lu_b0, pack_b0_tiles, pack_band_records, submatrix, swizzle_tile_rows, tile_span
+from .factor import (band_lu, lu_b0, pack_b0_tiles, pack_band_records, record_floor, submatrix, swizzle_tile_rows,
+                     tile_span)
 
 _DENSE_EIG_LIMIT = 1500
 
@@ -273,8 +274,10 @@ class TwoLevelPreconditioner:
         idx_off = [0]
         fwd_parts, bwd_parts, foff, boff = [], [], [], []
         fpos = bpos = 0
+        kl_floor = record_floor(max([f.kl for _, f in factors], default=0))
+        kv_floor = record_floor(max([f.kv for _, f in factors], default=0))
         for idof, f in factors:
-            fw, bw, fs, bs, klp, kvp = pack_band_records(f)
+            fw, bw, fs, bs, klp, kvp = pack_band_records(f, kl_floor, kv_floor)
             ns.append(f.n)
             kls.append(klp)
             kvs.append(kvp)

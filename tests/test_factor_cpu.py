@@ -69,3 +69,25 @@ def test_singular_block_is_named():
     blk = forms.helmholtz.tocsc()[idof][:, idof]
     with pytest.raises(hg.SingularOperatorError, match=r"\(0, 0\)"):
         factor.band_lu(blk, label=(0, 0))
+
+
+def test_record_floor_padding():
+    """Narrow blocks are zero padded to the launch's record floor: the padded
+    records still solve exactly (zero multipliers) and meet the floor."""
+    import numpy as np
+    import scipy.sparse as sp
+
+    from _helpers import emulate_band_records
+
+    assert factor.register_tiles(98) == 5 and factor.record_floor(98) == 95
+    assert factor.record_floor(24) <= 24 and factor.record_floor(2) == 0
+    rng = np.random.default_rng(3)
+    n, kl = 60, 4
+    A = sp.diags([rng.standard_normal(n - abs(d)) for d in range(-kl, kl + 1)], list(range(-kl, kl + 1))).tocsr()
+    A = A + sp.eye(n) * 3.0
+    f = factor.band_lu(A)
+    fwd, bwd, fs, bs, klp, kvp = factor.pack_band_records(f, kl_floor=31, kv_floor=40)
+    assert klp == 31 and kvp == 40 and fs >= 32 and bs >= 41
+    r = rng.standard_normal(n)
+    got = emulate_band_records(fwd.reshape(n, fs), bwd.reshape(n, bs), n, klp, kvp, r)
+    assert np.abs(got - f.solve(r)).max() <= 1e-12 * np.abs(f.solve(r)).max()

@@ -32,6 +32,9 @@ def cfg1(golden):
     return P, g, coarse, pre
 
 
+ORTHS = ["dcgs2", "measured"]
+
+
 def test_spmv_bitwise(cfg1):
     P, g, _, pre = cfg1
     assert np.array_equal(pre.spmv(g["u"], "B"), g["Bu"])
@@ -99,7 +102,21 @@ def test_local_solves_match_lapack(cfg1):
         assert rel(got, want) <= 1e-12
 
 
-ORTHS = ["dcgs2", "measured"]
+def test_local_solves_mixed_bandwidth():
+    """BASELINE config 4 (one level): boundary blocks are narrower (kl 47 vs
+    49, kv 94 vs 98) than the launch's register tiles; their zero-padded
+    records must give the host band LU's solution on every block."""
+    P = hg.build_problem("4", one_level=True)
+    pre = hg.factorize(P.forms, P.dec, None)
+    bands = {(f.lu.host.kl, f.lu.host.kv) for f in pre.local_solvers}
+    assert len(bands) > 1
+    rng = np.random.default_rng(40)
+    for ls in pre.local_solvers:
+        r = rng.standard_normal(ls.idof.size)
+        assert rel(ls.lu.solve(r), ls.lu.host.solve(r)) <= 1e-12
+    r = rng.standard_normal(pre.n)
+    orc = OraclePreconditioner(P.forms, P.dec, None)
+    assert rel(pre.apply(r), orc.apply(r)) <= APPLY_RTOL
 
 
 @pytest.mark.parametrize("orth", ORTHS)
