@@ -602,6 +602,7 @@ int hg_precond_destroy(HgPrecond* P) {
   release(P->d_b0_x);
   release(P->d_b0_done);
   release(P->d_zt_done);
+  release(P->d_blk_done);
   release(P->d_y);
   release(P->d_zs);
   release(P->d_cptr);
@@ -791,6 +792,9 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
     HG_TRY(upload<unsigned long long>(&P->d_zt_done, nullptr, 1, bytes));
     HG_CUDA_TRY(cudaMemset(P->d_zt_done, 0, sizeof(unsigned long long)));
     P->zt_epoch = 0;
+    HG_TRY(upload<unsigned long long>(&P->d_blk_done, nullptr, (size_t)D->n_cblk, bytes));
+    HG_CUDA_TRY(cudaMemset(P->d_blk_done, 0, sizeof(unsigned long long) * D->n_cblk));
+    P->zt_calls = 0;
     P->b0_epoch = 0;
     HG_TRY(upload<double>(&P->d_y, nullptr, (size_t)P->m, bytes));
     HG_TRY(upload<double>(&P->d_zs, nullptr, (size_t)std::max(nidx, 1LL), bytes));

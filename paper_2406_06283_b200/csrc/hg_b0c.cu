@@ -150,8 +150,8 @@ struct B0ClusterArgs {
   const double* tiles;      // swizzled, premultiplied [ntile][P][P]
   double* xbuf;             // [2][K*P] global copy of the solved panels
   double* y;
-  const unsigned long long* zt_done;  // Z^T r chunk counter; c is complete at zt_target
-  unsigned long long zt_target;
+  const unsigned long long* blk_done;  // per coarse block Z^T r chunk counters
+  unsigned long long zt_calls;         // block b of c is complete at zt_calls * nchunk_b
 };
 
 __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
@@ -174,12 +174,6 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
     }
     mbar_init(ldone, CS);
     fence_mbar_init();
-  }
-  if (tid == 0) {  // c = Z^T r of this apply complete (this kernel is launched before it)
-    unsigned long long v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.zt_done) : "memory");
-    } while (v < a.zt_target);
   }
   __syncthreads();
   cluster_sync_all();  // initialised rings and barriers before any remote access
@@ -215,8 +209,15 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
         if (q == 0) {
           double v = 0.0;
           if (i < a.m) {
+            // this kernel is launched before Z^T r: wait for this row's coarse block only
             const int col = a.perm[i];
-            const CblkDesc d = a.descs[a.col_blk[col]];
+            const int b = a.col_blk[col];
+            const CblkDesc d = a.descs[b];
+            const unsigned long long need = a.zt_calls * (unsigned long long)d.nchunk;
+            unsigned long long got;
+            do {
+              asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(got) : "l"(a.blk_done + b) : "memory");
+            } while (got < need);
             const int l = col - d.col0;
             for (int ch = 0; ch < d.nchunk; ++ch) v += a.cpart[d.part_off + (long long)ch * d.m + l];
           }
@@ -313,7 +314,7 @@ int launch_coarse_solve_cluster(HgPrecond* P, cudaStream_t st, unsigned long lon
   const int CS = P->b0_cs;
   B0ClusterArgs a{P->m, K, P->b0_nr, CS, P->d_b0_perm, P->d_col_blk, P->d_cblk, P->d_cpart, P->d_b0_dinv,
                   P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles, P->d_b0_x, P->d_y,
-                  P->d_zt_done, zt_target};
+                  P->d_blk_done, P->zt_calls + (zt_target > P->zt_epoch ? 1ull : 0ull)};
   const size_t smem = b0_cluster_smem(P->b0_nr);
   static size_t configured = 0;
   if (configured < smem) {

@@ -20,7 +20,8 @@ constexpr int ZT_ROWS = 256;
 __global__ void __launch_bounds__(256) k_zt(const int2* __restrict__ items, const CblkDesc* __restrict__ descs,
                                             const int* __restrict__ idx, const double* __restrict__ Z,
                                             const double* __restrict__ r, double* __restrict__ cpart,
-                                            unsigned long long* __restrict__ done) {
+                                            unsigned long long* __restrict__ done,
+                                            unsigned long long* __restrict__ blk_done) {
   __shared__ double s[4][64];
   const int2 it = items[blockIdx.x];
   const CblkDesc d = descs[it.x];
@@ -40,20 +41,23 @@ __global__ void __launch_bounds__(256) k_zt(const int2* __restrict__ items, cons
       cpart[d.part_off + (long long)chunk * d.m + col] = ((s[0][cl] + s[1][cl]) + s[2][cl]) + s[3][cl];
     __syncthreads();
   }
-  // completion count: the coarse solve, launched earlier on another stream so
-  // that it holds its SMs, starts when every chunk of this apply is counted
+  // completion counts: the coarse solve, launched earlier on another stream so
+  // that it holds its SMs, starts each panel as soon as the coarse blocks its
+  // rows come from are counted (per block), or waits for all (global)
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(done, 1ull);
+    atomicAdd(blk_done + it.x, 1ull);
   }
 }
 
 int launch_zt(HgPrecond* P, const double* r, cudaStream_t st) {
   if (P->m == 0 || P->n_zt_items == 0) return HG_OK;
   k_zt<<<P->n_zt_items, 256, 0, st>>>(P->d_zt_items, P->d_cblk, P->d_cblk_idx, P->d_z, r, P->d_cpart,
-                                        P->d_zt_done);
+                                        P->d_zt_done, P->d_blk_done);
   HG_LAUNCH_CHECK();
   P->zt_epoch += (unsigned long long)P->n_zt_items;
+  P->zt_calls += 1;
   return HG_OK;
 }
 
@@ -65,12 +69,24 @@ __global__ void __launch_bounds__(256) k_zy(const int2* __restrict__ items, cons
   const int k0 = it.y * ZT_ROWS, k1 = min(k0 + ZT_ROWS, d.n);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double* yb = y + d.col0;
-  for (int k = k0 + warp; k < k1; k += 8) {
-    const double* zr = Z + d.z_off + (long long)k * d.m;
-    double acc = 0.0;
-    for (int l = lane; l < d.m; l += 32) acc = fma(__ldg(zr + l), __ldg(yb + l), acc);
-    acc = warp_sum(acc);
-    if (lane == 0) zs[d.idx_off + k] = acc;
+  // a warp takes 4 rows at a time: all their loads in flight before the sums
+  for (int k = k0 + 4 * warp; k < k1; k += 32) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int l = lane; l < d.m; l += 32) {
+      const double yl = __ldg(yb + l);
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (k + t < k1) acc[t] = fma(__ldg(Z + d.z_off + (long long)(k + t) * d.m + l), yl, acc[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) acc[t] = warp_sum(acc[t]);
+    if (lane < 4 && k + lane < k1) {
+      double v = acc[0];
+#pragma unroll
+      for (int t = 1; t < 4; ++t)
+        if (lane == t) v = acc[t];
+      zs[d.idx_off + k + lane] = v;
+    }
   }
 }
 

@@ -77,6 +77,8 @@ struct HgPrecond {
   unsigned long long* d_zt_done = nullptr;  // monotone count of finished Z^T r chunks
   unsigned long long zt_epoch = 0;          // its value after the last launched Z^T r
   unsigned long long b0_zt_target = 0;      // chunks the next coarse solve waits for
+  unsigned long long* d_blk_done = nullptr; // per coarse block: monotone count of its finished single-RHS Z^T r chunks
+  unsigned long long zt_calls = 0;          // single-RHS Z^T r launches so far (block b is complete at zt_calls * nchunk_b)
   double* d_y = nullptr;          // coarse solution (m)
   long long zs_len = 0;
   double* d_zs = nullptr;         // per-block Z_b y_b rows (scratch)

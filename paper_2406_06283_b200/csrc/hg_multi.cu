@@ -794,7 +794,7 @@ int launch_dots2_batch(int n, const double* A, long long lda, const double* U, l
 //   q  = (V_c[j] - sum_{i<j} s_i V_c[i]) * rinv          (q_j re-orthogonalised)
 //   w  = w * rinv - sum_{i<j} c_i V_c[i] - c_j q          (w projected)
 // coef row of column c: [rinv, s_0..s_{j-1}, c_0..c_j].
-__global__ void __launch_bounds__(VEC_THREADS) k_dcgs2_update(int n, double* __restrict__ V, long long ldv,
+__global__ void __launch_bounds__(VEC_THREADS, 3) k_dcgs2_update(int n, double* __restrict__ V, long long ldv,
                                                               long long ldcol, int j, double* __restrict__ w,
                                                               long long ldw, const double* __restrict__ coef,
                                                               long long ldcoef, ColList cols) {
@@ -817,8 +817,27 @@ __global__ void __launch_bounds__(VEC_THREADS) k_dcgs2_update(int n, double* __r
     aq[k] = d < n ? Vc[(long long)j * ldv + d] : 0.0;
     aw[k] = d < n ? wc[d] * rinv : 0.0;
   }
-#pragma unroll 4
-  for (int i = 0; i < j; ++i) {  // sequential in i per row: fixed summation order
+  // chunks of 4 vectors: all 16 loads of a chunk issued before its FMAs;
+  // per row the sum stays sequential in i (fixed summation order)
+  int i = 0;
+  for (; i + 4 <= j; i += 4) {
+    double x[4][VEC_ROWS];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int k = 0; k < VEC_ROWS; ++k)
+        x[t][k] = rows[k] >= 0 ? __ldg(Vc + (long long)(i + t) * ldv + rows[k]) : 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const double si = sv[i + t], ci = cv[i + t];
+#pragma unroll
+      for (int k = 0; k < VEC_ROWS; ++k) {
+        aq[k] = fma(-si, x[t][k], aq[k]);
+        aw[k] = fma(-ci, x[t][k], aw[k]);
+      }
+    }
+  }
+  for (; i < j; ++i) {
     const double* vi = Vc + (long long)i * ldv;
     const double si = sv[i], ci = cv[i];
 #pragma unroll
