@@ -149,6 +149,13 @@ typedef struct {
   int32_t b0_mode;
   int32_t b0_cluster;
   int32_t b0_ring;
+  /* Optional dense B0^{-1} (m x m, row-major; NULL = none).  When given, the
+   * coarse solve is y = B0^{-1} c as an HBM-streaming GEMV (one right-hand
+   * side) / FP64 tensor-core GEMM (batches) that runs beside the local
+   * solves instead of the 2K-panel triangular chain.  The caller checks it
+   * against getrs (factorize does, bar 1e-11) — same operator, different
+   * rounding. */
+  const double* b0_inv;
 } HgPrecondDesc;
 
 /* ---- library ---- */

@@ -62,6 +62,7 @@ class HgPrecondDesc(ctypes.Structure):
         ("b0_mode", ctypes.c_int32),
         ("b0_cluster", ctypes.c_int32),
         ("b0_ring", ctypes.c_int32),
+        ("b0_inv", _f64p),
     ]
 
 

@@ -389,7 +389,15 @@ void stats_collect() {
 
 static int precond_apply_core(HgPrecond* P, const double* r, double* out, const double* W, long long ldw,
                               int nv, double* partials, int* nb, cudaStream_t st) {
-  if (P->m > 0) {
+  if (P->m > 0 && P->d_b0_inv) {
+    // dense coarse mode: Z^T r, then (side stream) c -> B0^{-1} c -> Z y beside the local solves
+    HG_TRY(launch_zt(P, r, st));
+    HG_CUDA_TRY(cudaEventRecord(P->ev_fork, st));
+    HG_CUDA_TRY(cudaStreamWaitEvent(P->aux, P->ev_fork, 0));
+    HG_TRY(launch_b0_dense(P, P->aux));
+    HG_TRY(launch_zy(P, P->aux));
+    HG_CUDA_TRY(cudaEventRecord(P->ev_join, P->aux));
+  } else if (P->m > 0) {
     HG_CUDA_TRY(cudaEventRecord(P->ev_fork, st));
     HG_CUDA_TRY(cudaStreamWaitEvent(P->aux, P->ev_fork, 0));
     if (serial_kernels()) {
@@ -410,6 +418,12 @@ static int precond_apply_core(HgPrecond* P, const double* r, double* out, const 
   HG_TRY(launch_local_solve(P, r, st));
   if (P->m > 0) HG_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_join, 0));
   return launch_assemble(P, true, true, out, W, ldw, nv, partials, nb, st);
+}
+
+// coarse solve of the current Z^T r partials on one stream (apply_coarse, profiling)
+static int coarse_solve_serial(HgPrecond* P, cudaStream_t st) {
+  if (P->d_b0_inv) return launch_b0_dense(P, st);
+  return launch_coarse_solve(P, st, P->zt_epoch);
 }
 
 // y = op(x); when partials != null also the fused dots of y against W[0..nv)
@@ -450,7 +464,14 @@ static int precond_apply_multi_core(HgPrecond* P, const double* R, long long ldr
     return HG_ERR_ARG;
   }
   HG_TRY(multi_prepare(P));
-  if (P->m > 0) {
+  if (P->m > 0 && P->d_b0_inv) {
+    HG_TRY(launch_zt_multi(P, R, ldr, nrhs, st));
+    HG_CUDA_TRY(cudaEventRecord(P->ev_fork, st));
+    HG_CUDA_TRY(cudaStreamWaitEvent(P->aux, P->ev_fork, 0));
+    HG_TRY(launch_b0_dense_multi(P, nrhs, P->aux));
+    HG_TRY(launch_zy_multi(P, nrhs, P->aux));
+    HG_CUDA_TRY(cudaEventRecord(P->ev_join, P->aux));
+  } else if (P->m > 0) {
     HG_CUDA_TRY(cudaEventRecord(P->ev_fork, st));
     HG_CUDA_TRY(cudaStreamWaitEvent(P->aux, P->ev_fork, 0));
     if (serial_kernels()) {
@@ -604,6 +625,10 @@ int hg_precond_destroy(HgPrecond* P) {
   release(P->d_zt_done);
   release(P->d_blk_done);
   release(P->d_y);
+  release(P->d_b0_inv);
+  release(P->d_c);
+  release(P->d_cm);
+  release(P->d_ypart);
   release(P->d_zs);
   release(P->d_cptr);
   release(P->d_cent);
@@ -797,6 +822,10 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
     P->zt_calls = 0;
     P->b0_epoch = 0;
     HG_TRY(upload<double>(&P->d_y, nullptr, (size_t)P->m, bytes));
+    if (D->b0_inv) {
+      HG_TRY(upload(&P->d_b0_inv, D->b0_inv, (size_t)P->m * P->m, bytes));
+      HG_TRY(upload<double>(&P->d_c, nullptr, (size_t)P->m, bytes));
+    }
     HG_TRY(upload<double>(&P->d_zs, nullptr, (size_t)std::max(nidx, 1LL), bytes));
     std::vector<int> ptr;
     std::vector<long long> ent;
@@ -812,6 +841,7 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
   HG_TRY(preload_multi());
   HG_TRY(preload_dcgs2());
   HG_TRY(preload_add());
+  HG_TRY(preload_b0_dense());
   HG_CUDA_TRY(cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking));
   HG_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
   HG_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
@@ -863,7 +893,7 @@ int hg_precond_apply_coarse(HgPrecond* P, const double* r, double* out, void* st
   cudaStream_t st = (cudaStream_t)stream;
   if (P->m == 0) return launch_fill(P->n, out, 0.0, st);
   HG_TRY(launch_zt(P, r, st));
-  HG_TRY(launch_coarse_solve(P, st, P->zt_epoch));
+  HG_TRY(coarse_solve_serial(P, st));
   HG_TRY(launch_zy(P, st));
   return launch_assemble(P, true, false, out, nullptr, 0, 0, nullptr, nullptr, st);
 }
@@ -883,7 +913,7 @@ int hg_precond_profile(HgPrecond* P, const double* r, double* out, int32_t iters
     cudaEventRecord(ev[0], st);
     if ((status = launch_zt(P, r, st)) != HG_OK) break;
     cudaEventRecord(ev[1], st);
-    if ((status = launch_coarse_solve(P, st, P->zt_epoch)) != HG_OK) break;
+    if ((status = coarse_solve_serial(P, st)) != HG_OK) break;
     cudaEventRecord(ev[2], st);
     if ((status = launch_zy(P, st)) != HG_OK) break;
     cudaEventRecord(ev[3], st);
@@ -932,7 +962,9 @@ int hg_precond_profile_multi(HgPrecond* P, const double* R, int64_t ldr, double*
     cudaEventRecord(ev[0], st);
     if ((status = launch_zt_multi(P, R, ldr, nrhs, st)) != HG_OK) break;
     cudaEventRecord(ev[1], st);
-    if ((status = launch_b0_multi(P, nrhs, st, P->zt_epoch)) != HG_OK) break;
+    if ((status = (P->d_b0_inv ? launch_b0_dense_multi(P, nrhs, st) : launch_b0_multi(P, nrhs, st, P->zt_epoch))) !=
+        HG_OK)
+      break;
     cudaEventRecord(ev[2], st);
     if ((status = launch_zy_multi(P, nrhs, st)) != HG_OK) break;
     cudaEventRecord(ev[3], st);

@@ -80,6 +80,10 @@ struct HgPrecond {
   unsigned long long* d_blk_done = nullptr; // per coarse block: monotone count of its finished single-RHS Z^T r chunks
   unsigned long long zt_calls = 0;          // single-RHS Z^T r launches so far (block b is complete at zt_calls * nchunk_b)
   double* d_y = nullptr;          // coarse solution (m)
+  double* d_b0_inv = nullptr;     // dense B0^{-1} (m x m row-major) or null
+  double* d_c = nullptr;          // reduced Z^T r (m), dense mode
+  double* d_cm = nullptr;         // [m][16] reduced Z^T R, dense mode
+  double* d_ypart = nullptr;      // [B0_KSPLIT][m][16] split-K partials, dense batched mode
   long long zs_len = 0;
   double* d_zs = nullptr;         // per-block Z_b y_b rows (scratch)
   int* d_cptr = nullptr;
@@ -193,6 +197,11 @@ int launch_spmm_self(const DevCsr& A, const double* vals, const double* X, long 
                      long long ldy, int nrhs, double* partials, int width, int* nblocks_out, cudaStream_t st);
 int launch_zt_multi(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st);
 int launch_b0_multi(HgPrecond* P, int nrhs, cudaStream_t st, unsigned long long zt_target);
+// dense coarse mode (hg_b0d.cu): c = reduce(Z^T r partials), y = B0^{-1} c
+int launch_b0_dense(HgPrecond* P, cudaStream_t st);
+int launch_b0_dense_multi(HgPrecond* P, int nrhs, cudaStream_t st);
+int preload_b0_dense();
+constexpr int B0_KSPLIT = 4;
 int launch_zy_multi(HgPrecond* P, int nrhs, cudaStream_t st);
 int launch_assemble_multi(HgPrecond* P, bool with_coarse, bool with_local, double* OUT, long long ldo, int nrhs,
                           cudaStream_t st);

@@ -335,6 +335,27 @@ class TwoLevelPreconditioner:
             self.b0_tiles = T
             self.b0_tile_dev = dev
             self.b0_bytes = T.nbytes + 4 * m + 4 * T.tile_col.size
+            # dense mode: B0^{-1} applied as a streaming GEMV / DMMA GEMM beside the
+            # local solves; kept only if it agrees with getrs (the reference's lu_solve)
+            self.b0_dense = False
+            self.b0_dense_dev = None
+            dense = os.environ.get("HG_B0_DENSE", "0")  # measured slower by default: see DESIGN.md section 8
+            if dense == "1" or (dense == "auto" and m <= 20000):  # "auto": whenever it fits
+                torch = _torch()
+                B0 = np.ascontiguousarray(np.asarray(self._coarse.B0), dtype=np.float64)
+                Binv = torch.linalg.inv(torch.from_numpy(B0).cuda())
+                Binv = np.ascontiguousarray(Binv.cpu().numpy())
+                rng = np.random.default_rng(1)
+                ddev = 0.0
+                for _ in range(2):
+                    c = rng.standard_normal(m)
+                    want = scipy.linalg.lu_solve((lu, piv), c)
+                    ddev = max(ddev, float(np.abs(Binv @ c - want).max() / max(np.abs(want).max(), 1e-300)))
+                self.b0_dense_dev = ddev
+                if ddev <= 1e-11:
+                    self.b0_dense = True
+                    d.b0_inv = arr(Binv, np.float64, f64)
+                    self.b0_bytes = 8 * m * m + 16 * m
             d.n_cblk = len(cblocks)
             d.cblk_n = arr([i.size for i, _ in cblocks], np.int32, i32)
             d.cblk_m = arr([b.shape[1] for _, b in cblocks], np.int32, i32)

@@ -98,8 +98,9 @@ def test_apply_multi_unpremultiplied_coarse_tiles(cfg1, monkeypatch):
     """The batched coarse solve on the L2-counter tile layout (b0 mode 0)."""
     P, g, coarse, _ = cfg1
     monkeypatch.setenv("HG_B0_MODE", "0")
+    monkeypatch.setenv("HG_B0_DENSE", "0")
     pre0 = hg.factorize(P.forms, P.dec, coarse)
-    assert pre0.b0_mode == 0
+    assert pre0.b0_mode == 0 and not pre0.b0_dense
     R = np.random.default_rng(9).standard_normal((pre0.n, 16))
     R[:, 5] = g["r"]
     got = pre0.apply_multi(R)
@@ -192,3 +193,26 @@ def test_config_batch_parity_vs_oracle(name):
         assert reps[c].converged and info["converged"]
         assert abs(reps[c].iterations - info["iterations"]) <= 1
         assert rel(X[:, c], xo) <= SOL_RTOL
+
+
+@pytest.mark.parametrize("name", ["1", "2"])
+def test_coarse_solve_modes_agree(name, monkeypatch):
+    """Dense B0^{-1} (GEMV / DMMA GEMM), the DSMEM cluster chain and the
+    batched tagged-pair chain: the same coarse operator to rounding, each
+    against the oracle (lu_solve, schwarz.py:56)."""
+    P = hg.build_problem(name)
+    orc = OraclePreconditioner(P.forms, P.dec, P.coarse)
+    R = np.random.default_rng(31).standard_normal((P.forms.n_dofs, 16))
+    outs = {}
+    for dense in ("1", "0"):
+        monkeypatch.setenv("HG_B0_DENSE", dense)
+        pre = hg.factorize(P.forms, P.dec, P.coarse)
+        assert pre.b0_dense == (dense == "1")
+        single = np.stack([pre.apply_coarse(R[:, c]) for c in (0, 9)], axis=1)
+        outs[dense] = (pre.apply(R[:, 0]), pre.apply_multi(R), single)
+        for k, c in enumerate((0, 9)):
+            assert rel(single[:, k], orc.apply_coarse(R[:, c])) <= APPLY_RTOL
+        assert rel(outs[dense][0], orc.apply(R[:, 0])) <= APPLY_RTOL
+        assert colrel(outs[dense][1], np.stack([pre.apply(R[:, c]) for c in range(16)], axis=1)) <= 1e-12
+    assert rel(outs["1"][0], outs["0"][0]) <= 1e-12
+    assert colrel(outs["1"][1], outs["0"][1]) <= 1e-12
