@@ -330,7 +330,11 @@ def run_ours(args, dist):
     ach = dbytes / (dms / 1e3) / 1e9 if dms > 0 else None
     roofline = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1) if ach else None, "peak": peak,
                 "unit": "GB/s", "frac": round(ach / peak, 4) if ach else None, "traffic": ncu_traffic(dom),
-                "peak_source": peak_src, "algorithmic_bytes_per_launch": int(dbytes / max(launches_dom, 1)),
+                "peak_source": peak_src,
+                "frac_of_8TBps_nominal": round(ach / 8000.0, 4) if ach else None,
+                "note": "peak = measured read+write copy burst; a read-dominated stream (the dots read the basis "
+                        "once and write nothing per row) can exceed it. traffic: ncu full captures of the DCGS2 "
+                        "kernels crash the profiled process on this pool (DESIGN.md section 8)", "algorithmic_bytes_per_launch": int(dbytes / max(launches_dom, 1)),
                 "ms_per_launch": round(dms / max(launches_dom, 1), 4), "launches": launches_dom,
                 "share_of_step": round(dms / ms_local, 4),
                 "phases_ms": {k: round(v, 1) for k, v in phase_ms.items()}}
