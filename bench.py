@@ -328,13 +328,17 @@ def run_ours(args, dist):
     dms, dbytes = cand[dom]
     launches_dom = phase_cnt["proj_dots" if dom == "k_dots2_batch" else "cgs_update"]
     ach = dbytes / (dms / 1e3) / 1e9 if dms > 0 else None
+    tr = ncu_traffic(dom)  # ncu DRAM bytes / algorithmic bytes of this kernel (profiles/ncu_traffic.json)
+    traffic = int(tr["ratio"] * dbytes / max(launches_dom, 1)) if tr else None
     roofline = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1) if ach else None, "peak": peak,
-                "unit": "GB/s", "frac": round(ach / peak, 4) if ach else None, "traffic": ncu_traffic(dom),
+                "unit": "GB/s", "frac": round(ach / peak, 4) if ach else None, "traffic": traffic,
+                "traffic_source": ("ncu dram__bytes_read.sum + dram__bytes_write.sum at j=%d (%s): %.3f x the "
+                                   "algorithmic bytes, scaled to this run's mean launch" % (tr["j"], tr["source"], tr["ratio"]))
+                if tr else None,
                 "peak_source": peak_src,
                 "frac_of_8TBps_nominal": round(ach / 8000.0, 4) if ach else None,
                 "note": "peak = measured read+write copy burst; a read-dominated stream (the dots read the basis "
-                        "once and write nothing per row) can exceed it. traffic: ncu full captures of the DCGS2 "
-                        "kernels crash the profiled process on this pool (DESIGN.md section 8)", "algorithmic_bytes_per_launch": int(dbytes / max(launches_dom, 1)),
+                        "once and write nothing per row) can exceed it", "algorithmic_bytes_per_launch": int(dbytes / max(launches_dom, 1)),
                 "ms_per_launch": round(dms / max(launches_dom, 1), 4), "launches": launches_dom,
                 "share_of_step": round(dms / ms_local, 4),
                 "phases_ms": {k: round(v, 1) for k, v in phase_ms.items()}}
