@@ -116,9 +116,9 @@ SIGNATURES = {
 }
 
 ABI_VERSION = 2
-NPHASES = 6
+NPHASES = 7  # HG_NPHASES
 ORTH = {"measured": 0, "dcgs2": 1}
-PHASES = ("op_apply", "proj_dots", "cgs_update", "measure", "second_pass", "append")
+PHASES = ("op_apply", "proj_dots", "cgs_update", "measure", "second_pass", "append", "w_spmv")
 MAX_RHS = 16
 
 _LIB = None

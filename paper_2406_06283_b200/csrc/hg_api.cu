@@ -639,6 +639,7 @@ int hg_precond_destroy(HgPrecond* P) {
   release(P->d_ym);
   release(P->d_b0m_x);
   release(P->d_b0m_done);
+  release(P->d_blkm_done);
   release(P->d_tmpm);
   if (P->aux) cudaStreamDestroy(P->aux);
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);
@@ -1535,13 +1536,19 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
         cf[1 + i] = s[i];
         sz += s[i] * z[i];
       }
+      // (H s)_i over the corrected columns 0..j-1, column by column (contiguous
+      // inner loops; summed in ascending column order for every row)
+      std::vector<double> hs(j + 1, 0.0);
+      for (int kk = 0; kk < j; ++kk) {
+        const double sk = s[kk];
+        const double* hk = S.Hraw[kk].data();
+        for (int i = 0; i <= kk + 1; ++i) hs[i] += hk[i] * sk;
+      }
       for (int i = 0; i <= j; ++i) {
-        double hs = 0.0;  // (H s)_i over the corrected columns 0..j-1
-        for (int kk = std::max(0, i - 1); kk < j; ++kk) hs += S.Hraw[kk][i] * s[kk];
         const double zp = (i < j) ? z[i] : (z[j] - sz) / rho;
-        const double h = (zp - hs) / rho;
+        const double h = (zp - hs[i]) / rho;
         col[i] = h;
-        cf[1 + j + i] = hs / rho + h;
+        cf[1 + j + i] = hs[i] / rho + h;
       }
       S.Hraw.push_back(col);
       keep.c[keep.n++] = c;

@@ -79,6 +79,8 @@ struct HgPrecond {
   unsigned long long b0_zt_target = 0;      // chunks the next coarse solve waits for
   unsigned long long* d_blk_done = nullptr; // per coarse block: monotone count of its finished single-RHS Z^T r chunks
   unsigned long long zt_calls = 0;          // single-RHS Z^T r launches so far (block b is complete at zt_calls * nchunk_b)
+  unsigned long long* d_blkm_done = nullptr;  // the same for the batched Z^T R
+  unsigned long long ztm_calls = 0;
   double* d_y = nullptr;          // coarse solution (m)
   double* d_b0_inv = nullptr;     // dense B0^{-1} (m x m row-major) or null
   double* d_c = nullptr;          // reduced Z^T r (m), dense mode

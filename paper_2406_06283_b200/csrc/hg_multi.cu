@@ -124,7 +124,8 @@ int launch_spmm_self(const DevCsr& A, const double* vals, const double* X, long 
 __global__ void __launch_bounds__(256) k_zt_multi(const int2* __restrict__ items, const CblkDesc* __restrict__ descs,
                                                   const int* __restrict__ idx, const double* __restrict__ Z,
                                                   const double* __restrict__ R, long long ldr, int nrhs,
-                                                  double* __restrict__ cpartm, unsigned long long* __restrict__ done) {
+                                                  double* __restrict__ cpartm, unsigned long long* __restrict__ done,
+                                                  unsigned long long* __restrict__ blk_done) {
   __shared__ __align__(16) double s_r[ZROWS * SR];
   const int2 it = items[blockIdx.x];
   const CblkDesc d = descs[it.x];
@@ -159,15 +160,17 @@ __global__ void __launch_bounds__(256) k_zt_multi(const int2* __restrict__ items
   if (threadIdx.x == 0) {  // chunk complete: the batched coarse solve may be waiting for it
     __threadfence();
     atomicAdd(done, 1ull);
+    atomicAdd(blk_done + it.x, 1ull);
   }
 }
 
 int launch_zt_multi(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st) {
   if (P->m == 0 || P->n_zt_items == 0) return HG_OK;
   k_zt_multi<<<P->n_zt_items, 256, 0, st>>>(P->d_zt_items, P->d_cblk, P->d_cblk_idx, P->d_z, R, ldr, nrhs,
-                                             P->d_cpartm, P->d_zt_done);
+                                             P->d_cpartm, P->d_zt_done, P->d_blkm_done);
   HG_LAUNCH_CHECK();
   P->zt_epoch += (unsigned long long)P->n_zt_items;
+  P->ztm_calls += 1;
   return HG_OK;
 }
 
@@ -281,8 +284,8 @@ struct B0MultiArgs {
   double* xbuf;             // [2K][64][MR] (value, tag) pairs: 2 doubles each
   double* y;                // [m][MR]
   double tag0;              // tag of panel g in this launch: tag0 + g (unique across launches)
-  const unsigned long long* zt_done;
-  unsigned long long zt_target;
+  const unsigned long long* blk_done;  // per coarse block Z^T R chunk counters
+  unsigned long long zt_calls;         // block b complete at zt_calls * nchunk_b
 };
 
 // 16-byte (value, tag) pair access: written and read as one vector access,
@@ -336,10 +339,6 @@ __global__ void __launch_bounds__(256, 1) k_b0_multi(B0MultiArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = lane & 3, g8 = lane >> 2;
   const int row = warp * 8 + g8;
   const int K = a.K;
-  if (tid == 0)
-    while (ld_acq(a.zt_done) < a.zt_target) {
-    }
-  __syncthreads();
   for (int g = blockIdx.x; g < 2 * K; g += gridDim.x) {
     const int ph = g / K, t = g % K;
     const double* dinv_g = a.dinv + (size_t)g * BTILE;
@@ -352,8 +351,13 @@ __global__ void __launch_bounds__(256, 1) k_b0_multi(B0MultiArgs a) {
         double v = 0.0;
         const int i = t * BP + r;
         if (c < a.nrhs && i < a.m) {
+          // launched before Z^T R: wait for this row's coarse block only
           const int col = a.perm[i];
-          const CblkDesc d = a.descs[a.col_blk[col]];
+          const int b = a.col_blk[col];
+          const CblkDesc d = a.descs[b];
+          const unsigned long long need = a.zt_calls * (unsigned long long)d.nchunk;
+          while (ld_acq(a.blk_done + b) < need) {
+          }
           const int l = col - d.col0;
           for (int ch = 0; ch < d.nchunk; ++ch) v += a.cpartm[(d.part_off + (long long)ch * d.m + l) * MR + c];
         }
@@ -420,7 +424,8 @@ int launch_b0_multi(HgPrecond* P, int nrhs, cudaStream_t st, unsigned long long 
   // tags stay below 2^53 (exact in a double) for ~10^12 launches
   B0MultiArgs a{P->m, K, nrhs, P->b0_mode == 1 ? 1 : 0, P->b0_mode == 1 ? 1 : 0, P->d_b0_perm, P->d_col_blk,
                 P->d_cblk, P->d_cpartm, P->d_b0_dinv, P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles,
-                P->d_b0m_x, P->d_ym, (double)(P->b0m_epoch + 1), P->d_zt_done, zt_target};
+                P->d_b0m_x, P->d_ym, (double)(P->b0m_epoch + 1), P->d_blkm_done,
+                P->ztm_calls + (zt_target > P->zt_epoch ? 1ull : 0ull)};
   P->b0m_epoch += 2ull * K;
   k_b0_multi<<<G, 256, 0, st>>>(a);
   HG_LAUNCH_CHECK();
@@ -614,6 +619,9 @@ int multi_prepare(HgPrecond* P) {
       HG_TRY(alloc(&P->d_cm, (size_t)MR * P->m));
       HG_TRY(alloc(&P->d_ypart, (size_t)B0_KSPLIT * MR * P->m));
     }
+    HG_CUDA_TRY(cudaMalloc(&P->d_blkm_done, sizeof(unsigned long long) * P->n_cblk));
+    HG_CUDA_TRY(cudaMemset(P->d_blkm_done, 0, sizeof(unsigned long long) * P->n_cblk));
+    P->ztm_calls = 0;
     HG_CUDA_TRY(cudaMalloc(&P->d_b0m_done, sizeof(unsigned long long)));
     HG_CUDA_TRY(cudaMemset(P->d_b0m_done, 0, sizeof(unsigned long long)));
     P->b0m_epoch = 0;

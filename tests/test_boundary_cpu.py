@@ -41,3 +41,16 @@ def test_product_never_imports_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle\b", src, flags=re.M), f
+
+
+def test_python_constants_match_header():
+    """Host arrays sized from _lib must match the header's sizes."""
+    from paper_2406_06283_b200 import _lib
+
+    text = open(os.path.join(ROOT, "include", "helmgpu.h")).read()
+    consts = dict(re.findall(r"#define (HG_[A-Z0-9_]+) (\d+)", text))
+    assert int(consts["HG_NPHASES"]) == _lib.NPHASES == len(_lib.PHASES)
+    assert int(consts["HG_MAX_RHS"]) == _lib.MAX_RHS
+    assert int(consts["HG_ABI_VERSION"]) == _lib.ABI_VERSION
+    assert int(consts["HG_ORTH_MEASURED"]) == _lib.ORTH["measured"]
+    assert int(consts["HG_ORTH_DCGS2"]) == _lib.ORTH["dcgs2"]
