@@ -4,6 +4,8 @@
 // the host, as the north star prescribes).
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -1367,9 +1369,18 @@ static int weight_csr(HgOp* wop, const DevCsr** A, const double** vals) {
   return HG_OK;
 }
 
+// HG_HOST_TIMING=1: report the host's share of the DCGS2 loop (diagnosis)
+static bool host_timing() {
+  static const bool on = getenv("HG_HOST_TIMING") && getenv("HG_HOST_TIMING")[0] == '1';
+  return on;
+}
+static double g_host_wait = 0.0, g_host_work = 0.0;
+
 static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr, double* x, long long ldx, int nrhs,
                        double rtol, int maxit, double* history, int32_t* info, cudaStream_t st) {
   const int n = op->n;
+  const auto t_start = std::chrono::steady_clock::now();
+  g_host_wait = g_host_work = 0.0;
   const bool weighted = weight != nullptr;
   const DevCsr* WA = nullptr;
   const double* wvals = nullptr;
@@ -1480,20 +1491,26 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
     }
     {
       Phase ph(st, 1);
+      // compact [c][2 nv] rows: one contiguous D2H per iteration
       HG_TRY(launch_dots2_batch(n, weighted ? ws.wq : qv(j), n, U, n, Q, vstride, n, nv, act, ws.partials, ws.dots,
-                                W2, st));
+                                2 * nv, st));
     }
-    HG_CUDA_TRY(cudaMemcpy2DAsync(hdots, sizeof(double) * W2, ws.dots, sizeof(double) * W2, sizeof(double) * 2 * nv,
-                                  nrhs, cudaMemcpyDeviceToHost, st));
+    HG_CUDA_TRY(cudaMemcpyAsync(hdots, ws.dots, sizeof(double) * 2 * nv * nrhs, cudaMemcpyDeviceToHost, st));
     HG_CUDA_TRY(cudaMemcpyAsync(hnrm, ws.nrm2, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, st));
+    const auto th0 = std::chrono::steady_clock::now();
     HG_CUDA_TRY(cudaStreamSynchronize(st));
+    const auto th1 = std::chrono::steady_clock::now();
 
     ColList keep{}, done{};
+    int stopped[HG_MAX_RHS];
+    // columns are independent: their host work (Givens, H s) runs in parallel
+#pragma omp parallel for schedule(static, 1) num_threads(act.n) if (act.n >= 4)
     for (int k = 0; k < act.n; ++k) {
       const int c = act.c[k];
+      stopped[k] = 0;
       ColState& S = cst[c];
-      const double* a = hdots + c * W2;  // Q_i . W q_j
-      const double* z = a + nv;          // Q_i . W w
+      const double* a = hdots + (long long)c * 2 * nv;  // Q_i . W q_j
+      const double* z = a + nv;                         // Q_i . W w
       double rho = 1.0;
       std::vector<double> s(j, 0.0);
       bool stop = false;
@@ -1524,12 +1541,12 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
       }
       if (!stop && j == maxit) stop = true;  // maxit columns finalised, not converged
       if (stop) {
-        done.c[done.n++] = c;
+        stopped[k] = 1;
         continue;
       }
       // projection of A q_j (q_j corrected) onto Q_{0:j}
       std::vector<double> col(j + 2, 0.0);
-      double* cf = hcoef + c * W2;
+      double* cf = hcoef + (long long)c * (2 * j + 2);  // compact rows: one contiguous H2D
       cf[0] = 1.0 / rho;
       double sz = 0.0;
       for (int i = 0; i < j; ++i) {
@@ -1551,15 +1568,24 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
         cf[1 + j + i] = hs[i] / rho + h;
       }
       S.Hraw.push_back(col);
-      keep.c[keep.n++] = c;
+    }
+    for (int k = 0; k < act.n; ++k) {
+      if (stopped[k])
+        done.c[done.n++] = act.c[k];
+      else
+        keep.c[keep.n++] = act.c[k];
     }
     if (keep.n > 0 || done.n > 0) HG_TRY(ws.Q.ensure(vbytes * nrhs * std::min(j + 2, ws.cap)));
+    const auto th2 = std::chrono::steady_clock::now();
+    if (host_timing()) {
+      g_host_wait += std::chrono::duration<double>(th1 - th0).count();
+      g_host_work += std::chrono::duration<double>(th2 - th1).count();
+    }
     if (keep.n > 0) {
-      HG_CUDA_TRY(cudaMemcpy2DAsync(ws.coef, sizeof(double) * W2, hcoef, sizeof(double) * W2,
-                                    sizeof(double) * (2 * j + 2), nrhs, cudaMemcpyHostToDevice, st));
+      HG_CUDA_TRY(cudaMemcpyAsync(ws.coef, hcoef, sizeof(double) * (2 * j + 2) * nrhs, cudaMemcpyHostToDevice, st));
       {
         Phase ph(st, 2);
-        HG_TRY(launch_dcgs2_update(n, Q, vstride, n, j, ws.w, n, ws.coef, W2, keep, st));
+        HG_TRY(launch_dcgs2_update(n, Q, vstride, n, j, ws.w, n, ws.coef, 2 * j + 2, keep, st));
       }
       {
         Phase ph(st, 3);
@@ -1605,6 +1631,11 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
   }
   HG_CUDA_TRY(cudaStreamSynchronize(st));
   stats_collect();
+  if (host_timing()) {
+    const double tot = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    fprintf(stderr, "[dcgs2 host] nrhs %d: total %.1f ms, waiting at the per-iteration sync %.1f ms, host work "
+            "after it %.1f ms\n", nrhs, tot * 1e3, g_host_wait * 1e3, g_host_work * 1e3);
+  }
   for (int c = 0; c < nrhs; ++c) {
     info[4 * c] = mlist[c];
     info[4 * c + 1] = cst[c].converged ? 1 : 0;
