@@ -1385,6 +1385,16 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
   const DevCsr* WA = nullptr;
   const double* wvals = nullptr;
   if (weighted) HG_TRY(weight_csr(weight, &WA, &wvals));
+  // Y = W X for the listed columns (+ self dots X.Y into pself[c][nb] when given);
+  // one column runs the single-vector SpMV kernels
+  auto wspmv = [&](const double* X, double* Y, const ColList& cols, double* pself, int* nbs) -> int {
+    if (nrhs == 1) {
+      if (cols.n == 0) return HG_OK;
+      if (pself) return launch_spmv_dots(*WA, wvals, X, Y, nullptr, 0, 0, false, pself, nbs, st);
+      return launch_spmv(*WA, wvals, X, Y, st);
+    }
+    return launch_spmm_cols(*WA, wvals, X, n, Y, n, cols, pself, pself ? 1 : 0, nbs, st);
+  };
   DcWs& ws = nrhs == 1 ? op->dws : op->dwsb;
   HG_TRY(dws_reserve(ws, n, nrhs, maxit + 1, weighted));
   const long long W2 = 2LL * (ws.cap + 2), Y2 = ws.cap + 2;
@@ -1407,7 +1417,7 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
   // q_0 = r0 / ||r0||_W (wgmres.py:102-115)
   HG_CUDA_TRY(cudaMemcpy2DAsync(Q, vbytes, rhs, sizeof(double) * ldr, vbytes, nrhs, cudaMemcpyDeviceToDevice, st));
   if (weighted) {
-    HG_TRY(launch_spmm_cols(*WA, wvals, Q, n, ws.wq, n, all, ws.pself, 1, &nbs, st));
+    HG_TRY(wspmv(Q, ws.wq, all, ws.pself, &nbs));
     HG_TRY(launch_reduce_batch(ws.pself, nbs, 1, 1, all, ws.nrm2, 1, st));
   } else {
     HG_TRY(launch_dots_batch(n, Q, n, nullptr, 0, 0, 0, all, ws.partials, 1, &nb, st));
@@ -1486,7 +1496,7 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
     const double* U = ws.w;
     if (weighted) {
       Phase ph(st, 6);
-      HG_TRY(launch_spmm_cols(*WA, wvals, ws.w, n, ws.u, n, act, nullptr, 0, nullptr, st));
+      HG_TRY(wspmv(ws.w, ws.u, act, nullptr, nullptr));
       U = ws.u;
     }
     {
@@ -1590,7 +1600,7 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
       {
         Phase ph(st, 3);
         if (weighted) {
-          HG_TRY(launch_spmm_cols(*WA, wvals, ws.w, n, ws.ww, n, keep, ws.pself, 1, &nbs, st));
+          HG_TRY(wspmv(ws.w, ws.ww, keep, ws.pself, &nbs));
           HG_TRY(launch_reduce_batch(ws.pself, nbs, 1, 1, keep, ws.nrm2, 1, st));
         } else {
           HG_TRY(launch_dots_batch(n, ws.w, n, nullptr, 0, 0, 0, keep, ws.partials, 1, &nb, st));
