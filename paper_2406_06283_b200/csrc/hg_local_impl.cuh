@@ -337,34 +337,44 @@ static LocalKernel pick2() {
     return k_local_solve_multi<RF, RB>;
 }
 
-// kv = kl + ku >= kl, so rb >= rf: only those tiles are instantiated
+// compile-time tile actually instantiated for a switch case (cases the
+// runtime guard below rejects map onto an instantiated one, never returned)
+constexpr int rb_clamp(int rf, int x, int nw) {
+  return x < rf ? rf : (nw > 1 && x > 2 * rf + 1 ? 2 * rf + 1 : x);
+}
+
+// kv = kl + ku >= kl, so rb >= rf: only those tiles are instantiated; the
+// batched kernel only for rb <= 2 rf + 1 (ku <= kl, as for the symmetric
+// band patterns of the Helmholtz blocks; anything else fails loudly)
 template <int RF, int NW>
 static LocalKernel pick_rb(int rb) {
-  if (rb < RF) return nullptr;
+  if (rb < RF || (NW > 1 && rb > 2 * RF + 1)) return nullptr;
   switch (rb) {
-    case 2: return pick2<RF, (RF <= 2 ? 2 : RF), NW>();
-    case 3: return pick2<RF, (RF <= 3 ? 3 : RF), NW>();
-    case 4: return pick2<RF, (RF <= 4 ? 4 : RF), NW>();
-    case 5: return pick2<RF, (RF <= 5 ? 5 : RF), NW>();
-    case 6: return pick2<RF, 6, NW>();
-    case 7: return pick2<RF, 7, NW>();
-    case 8: return pick2<RF, 8, NW>();
-    case 9: return pick2<RF, 9, NW>();
-    case 10: return pick2<RF, 10, NW>();
+    case 2: return pick2<RF, rb_clamp(RF, 2, NW), NW>();
+    case 3: return pick2<RF, rb_clamp(RF, 3, NW), NW>();
+    case 4: return pick2<RF, rb_clamp(RF, 4, NW), NW>();
+    case 5: return pick2<RF, rb_clamp(RF, 5, NW), NW>();
+    case 6: return pick2<RF, rb_clamp(RF, 6, NW), NW>();
+    case 7: return pick2<RF, rb_clamp(RF, 7, NW), NW>();
+    case 8: return pick2<RF, rb_clamp(RF, 8, NW), NW>();
+    case 9: return pick2<RF, rb_clamp(RF, 9, NW), NW>();
+    case 10: return pick2<RF, rb_clamp(RF, 10, NW), NW>();
     default: return nullptr;
   }
 }
 
+// Instantiations are spread over several translation units (hg_local_t*.cu)
+// so they compile in parallel; each defines one of these per-rf pickers.
+LocalKernel pick_local_single_lo(int rf, int rb);   // rf 2..3
+LocalKernel pick_local_single_hi(int rf, int rb);   // rf 4..6
+LocalKernel pick_local_multi_lo(int rf, int rb);    // rf 2..3
+LocalKernel pick_local_multi_mid(int rf, int rb);   // rf 4
+LocalKernel pick_local_multi_hi(int rf, int rb);    // rf 5..6
+
 template <int NW>
 static LocalKernel pick_local(int rf, int rb) {
-  switch (rf) {
-    case 2: return pick_rb<2, NW>(rb);
-    case 3: return pick_rb<3, NW>(rb);
-    case 4: return pick_rb<4, NW>(rb);
-    case 5: return pick_rb<5, NW>(rb);
-    case 6: return pick_rb<6, NW>(rb);
-    default: return nullptr;
-  }
+  if (NW == 1) return rf <= 3 ? pick_local_single_lo(rf, rb) : pick_local_single_hi(rf, rb);
+  return rf <= 3 ? pick_local_multi_lo(rf, rb) : rf == 4 ? pick_local_multi_mid(rf, rb) : pick_local_multi_hi(rf, rb);
 }
 
 // Launch the block solves of `nblocks` descriptors with nrhs consumer warps.
