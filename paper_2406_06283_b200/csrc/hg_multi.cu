@@ -651,41 +651,9 @@ int preload_multi() {
 // ------------------------------------------------------------------ DCGS2 Arnoldi kernels
 namespace hg {
 
-// Butterfly reduce-scatter of 16 per-lane values over a warp: afterwards
-// lane L holds the warp total of value ((L>>4)&1)*8 + ((L>>3)&1)*4 +
-// ((L>>2)&1)*2 + ((L>>1)&1) (16 shuffles instead of 16 x 5).
-__device__ __forceinline__ double warp_reduce16(double (&v)[16], int lane) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const bool hi = lane & 16;
-    const double send = hi ? v[i] : v[8 + i];
-    const double keep = hi ? v[8 + i] : v[i];
-    v[i] = keep + __shfl_xor_sync(FULL, send, 16);
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const bool hi = lane & 8;
-    const double send = hi ? v[i] : v[4 + i];
-    const double keep = hi ? v[4 + i] : v[i];
-    v[i] = keep + __shfl_xor_sync(FULL, send, 8);
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const bool hi = lane & 4;
-    const double send = hi ? v[i] : v[2 + i];
-    const double keep = hi ? v[2 + i] : v[i];
-    v[i] = keep + __shfl_xor_sync(FULL, send, 4);
-  }
-  {
-    const bool hi = lane & 2;
-    const double send = hi ? v[0] : v[1];
-    const double keep = hi ? v[1] : v[0];
-    v[0] = keep + __shfl_xor_sync(FULL, send, 2);
-  }
-  return v[0] + __shfl_xor_sync(FULL, v[0], 1);
-}
-
-// 8-value variant: lane L ends with the total of value ((L>>4)&1)*4 + ((L>>3)&1)*2 + ((L>>2)&1).
+// Butterfly reduce-scatter of 8 per-lane values over a warp (9 shuffles
+// instead of 8 x 5): afterwards lane L holds the warp total of value
+// ((L>>4)&1)*4 + ((L>>3)&1)*2 + ((L>>2)&1).
 __device__ __forceinline__ double warp_reduce8(double (&v)[8], int lane) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
