@@ -56,7 +56,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="5-16")
     ap.add_argument("--cpu-iters", type=int, default=6, help="GMRES iterations in the CPU baseline sample")
-    ap.add_argument("--ref-iters", type=int, default=3, help="GMRES iterations per reference-arm step")
+    ap.add_argument("--ref-iters", type=int, default=5, help="GMRES iterations per reference-arm step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cstab", default="cache", help="'cache' (recorded setup constant), 'auto' (recompute)")
@@ -478,7 +478,9 @@ def run_ours(args, dist):
 
 
 def cpu_baseline(P, pre, iters):
-    """The oracle (restated reference solve path) on a bounded sample of the workload."""
+    """The oracle (restated reference solve path) on a bounded sample of the
+    workload: `iters` GMRES iterations from rhs_p = M^-1 f (rhs_p computed
+    before the clock starts: it is one apply in a ~306-apply solve)."""
     from oracle.schwarz_oracle import OraclePreconditioner
     from oracle.wgmres_oracle import weighted_gmres as oracle_gmres
 
@@ -488,13 +490,12 @@ def cpu_baseline(P, pre, iters):
     B, Dk = P.forms.helmholtz, P.forms.dk
     t0 = time.perf_counter()
     rhs_p = orc.apply(f)
+    t_apply = time.perf_counter() - t0
+    t0 = time.perf_counter()
     x, info = oracle_gmres(lambda v: orc.apply(B @ v), rhs_p, weight=Dk, rtol=0.0, maxit=iters)
     dt = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    orc.apply(f)
-    t_apply = time.perf_counter() - t0
     return {"value": round(info["iterations"] / dt, 4), "unit": "iters/s", "cores": cores, "kind": "port",
-            "sample": "rhs_p = M^-1 f + %d GMRES iterations (fixed-iteration mode) of the same workload, "
+            "sample": "%d GMRES iterations (fixed-iteration mode) from rhs_p = M^-1 f of the same workload, "
                       "oracle/ restatement on SuperLU/LAPACK/numpy, default BLAS threads" % info["iterations"],
             "seconds": round(dt, 2), "apply_s": round(t_apply, 3)}
 
@@ -512,10 +513,13 @@ def run_reference(args, dist):
     log("reference-arm setup %.1f s" % (time.perf_counter() - t0))
     rhs = P.rhs if P.rhs.ndim == 2 else P.rhs[:, None]
     B, Dk = P.forms.helmholtz, P.forms.dk
+    nsteps = args.warmup + args.steps
+    # rhs_p = M^-1 f per column before the clock (one apply in a ~306-apply solve)
+    rhs_p = {c: orc.apply(rhs[:, c]) for c in sorted({s % rhs.shape[1] for s in range(nsteps)})}
 
     def step(s):
-        f = rhs[:, s % rhs.shape[1]]
-        x, info = oracle_gmres(lambda v: orc.apply(B @ v), orc.apply(f), weight=Dk, rtol=0.0, maxit=args.ref_iters)
+        x, info = oracle_gmres(lambda v: orc.apply(B @ v), rhs_p[s % rhs.shape[1]], weight=Dk, rtol=0.0,
+                               maxit=args.ref_iters)
         return info["iterations"]
 
     for s in range(args.warmup):
@@ -542,9 +546,11 @@ def run_reference(args, dist):
         "dtype": "f64",
         "data": "synthetic, seeded",
         "config": {"workload": "BASELINE config %s (same as the ours arm)" % P.config.name,
-                   "step": "rhs_p = M^-1 f + %d GMRES iterations, CPU oracle port" % args.ref_iters},
+                   "step": "%d GMRES iterations from rhs_p = M^-1 f (computed before the clock), CPU oracle port"
+                           % args.ref_iters},
         "cpu_baseline": {"value": round(value, 4), "unit": "iters/s", "cores": cores, "kind": "port",
-                         "sample": "%d GMRES iterations + 1 apply per step on the host cores" % args.ref_iters},
+                         "sample": "%d GMRES iterations per step on the host cores (oracle restatement of the "
+                                   "reference's SuperLU / LAPACK / numpy solve path)" % args.ref_iters},
         "e2e": {"value": round(value, 4), "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 

@@ -58,5 +58,6 @@ from .schwarz import (
     factorize,
 )
 from .wgmres import GmresReport, elman_gamma, weighted_gmres, weighted_gmres_batch
+from .analysis import fov_bounds
 
 __version__ = "0.1.0"

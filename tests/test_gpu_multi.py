@@ -216,3 +216,49 @@ def test_coarse_solve_modes_agree(name, monkeypatch):
         assert colrel(outs[dense][1], np.stack([pre.apply(R[:, c]) for c in range(16)], axis=1)) <= 1e-12
     assert rel(outs["1"][0], outs["0"][0]) <= 1e-12
     assert colrel(outs["1"][1], outs["0"][1]) <= 1e-12
+
+
+def _fov_reference_loop(forms, apply_T, mode, samples=0, rng=None):
+    """helmdd.analysis.fov_bounds (analysis.py:342-375) with a given apply_T."""
+    import scipy.linalg
+
+    Dk = forms.dk
+    n = forms.n_dofs
+    if mode == "dense":
+        T = np.empty((n, n))
+        eye = np.eye(n)
+        for j in range(n):
+            T[:, j] = apply_T(eye[:, j])
+        Dk_d = Dk.toarray()
+        M1 = Dk_d @ T
+        sym = 0.5 * (M1 + M1.T)
+        return (float(scipy.linalg.eigh(sym, Dk_d, eigvals_only=True)[0]),
+                float(scipy.linalg.eigh(T.T @ M1, Dk_d, eigvals_only=True)[-1]))
+    c1, c2 = np.inf, 0.0
+    for _ in range(samples):
+        u = rng.standard_normal(n)
+        tu = apply_T(u)
+        du = Dk @ u
+        denom = float(u @ du)
+        c1 = min(c1, float(tu @ du) / denom)
+        c2 = max(c2, float(tu @ (Dk @ tu)) / denom)
+    return c1, c2
+
+
+def test_fov_bounds_batched_matches_reference_loop(cfg1):
+    """the analysis consumer on batched device applies."""
+    P, g, _, pre = cfg1
+    got = hg.fov_bounds(P.forms, pre, mode="sampled", samples=40, rng=np.random.default_rng(5))
+    want = _fov_reference_loop(P.forms, pre.apply_T, "sampled", 40, np.random.default_rng(5))
+    assert abs(got[0] - want[0]) <= 1e-10 * abs(want[0]) and abs(got[1] - want[1]) <= 1e-10 * abs(want[1])
+    mesh = hg.build_unit_square_mesh(8)
+    space = hg.build_fe_space(mesh)
+    forms = hg.assemble_forms(mesh, space, hg.coefficient_field(mesh), 5.0)
+    dec = hg.build_two_level(mesh, space, 2, 2)
+    res = [hg.solve_indefinite_gevp(hg.assemble_local_gevp(i, forms, dec)) for i in range(dec.n_coarse)]
+    coarse = hg.build_coarse_space(res, hg.select_modes(res, 1.0), dec, forms)
+    small = hg.factorize(forms, dec, coarse)
+    orc = OraclePreconditioner(forms, dec, coarse)
+    got = hg.fov_bounds(forms, small, mode="dense")
+    want = _fov_reference_loop(forms, lambda u: orc.apply(forms.helmholtz @ u), "dense")
+    assert abs(got[0] - want[0]) <= 1e-9 * abs(want[0]) and abs(got[1] - want[1]) <= 1e-9 * abs(want[1])
