@@ -161,6 +161,9 @@ int spmv_dots_nblocks(int n);
 
 int launch_local_solve(HgPrecond* P, const double* r, cudaStream_t st);
 int launch_local_solve_multi(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st);
+// blocked multi-RHS local solve (hg_local_blk.cu): 32-row chains + DMMA band updates
+int launch_local_blocked(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st);
+int preload_local_blocked();
 int launch_local_solve_single(HgPrecond* P, int s, const double* r_local, double* x_local, cudaStream_t st);
 int launch_zt(HgPrecond* P, const double* r, cudaStream_t st);
 // zt_target: value of the Z^T r chunk counter the solve waits for before reading c
