@@ -59,6 +59,28 @@ struct BlkCtx {
   int stage_stride;
 };
 
+// one chain step s of a block for this lane's row rw and its warp's two columns
+template <bool FWD>
+__device__ __forceinline__ void blk_step(int s, const double* __restrict__ r, int rw, int kw, double& v0,
+                                         double& v1) {
+  const bool below = rw > s && rw - s <= kw;
+  const double m = below ? r[rw - s - 1] : 0.0;
+  double x0 = __shfl_sync(FULL, v0, s), x1 = __shfl_sync(FULL, v1, s);
+  if (!FWD) {
+    const double dv = r[kw];
+    x0 *= dv;
+    x1 *= dv;
+    if (rw == s) {
+      v0 = x0;
+      v1 = x1;
+    }
+  }
+  if (below) {
+    v0 = fma(-m, x0, v0);
+    v1 = fma(-m, x1, v1);
+  }
+}
+
 // one sweep (FWD: gathered input, pivoted L; !FWD: reversed U with 1/u_jj)
 template <bool FWD>
 __device__ void blk_sweep(const BlkCtx& cx, int& chunk, int n, int kw, int stride, const int* __restrict__ idx,
@@ -84,6 +106,11 @@ __device__ void blk_sweep(const BlkCtx& cx, int& chunk, int n, int kw, int strid
   for (int j0 = 0; j0 < n; j0 += BK) {
     const long long c0t = clock64();
     const int nb = min(BK, n - j0);
+    const int base = j0 % W;  // ring position of row j0: row j0 + x (0 <= x < W) sits at wr(x)
+    auto wr = [&](int x) -> int {
+      const int p = base + x;
+      return p >= W ? p - W : p;
+    };
     const int nch = (nb + BCH - 1) / BCH;
     // rows entering the window after this block (positions of the block's rows), fetched early
     double nxt[2];
@@ -118,29 +145,17 @@ __device__ void blk_sweep(const BlkCtx& cx, int& chunk, int n, int kw, int strid
       {
         const int rw = lane;  // block row of this lane
         const int c0 = 2 * warp;
-        double* wrow = win + ((j0 + rw) % W) * BSR + c0;
+        double* wrow = win + wr(rw) * BSR + c0;
         const double2 t2 = *reinterpret_cast<const double2*>(wrow);
         double v0 = t2.x, v1 = t2.y;
-#pragma unroll 8
-        for (int s = 0; s < nb; ++s) {
-          const double* r = rec(s);
-          const bool below = rw > s && rw - s <= kw;
-          const double m = below ? r[rw - s - 1] : 0.0;
-          double x0 = __shfl_sync(FULL, v0, s), x1 = __shfl_sync(FULL, v1, s);
-          if (!FWD) {
-            const double dv = r[kw];
-            x0 *= dv;
-            x1 *= dv;
-            if (rw == s) {
-              v0 = x0;
-              v1 = x1;
-            }
-          }
-          if (below) {
-            v0 = fma(-m, x0, v0);
-            v1 = fma(-m, x1, v1);
-          }
-        }
+        // step s of the block: record rec0 + s*stride (s < 16) / rec1 + (s-16)*stride
+        const int n0 = min(nb, BCH);
+        const double* r = rec0;
+#pragma unroll 4
+        for (int s = 0; s < n0; ++s, r += stride) blk_step<FWD>(s, r, rw, kw, v0, v1);
+        r = rec1;
+#pragma unroll 4
+        for (int s = BCH; s < nb; ++s, r += stride) blk_step<FWD>(s, r, rw, kw, v0, v1);
         if (rw < nb) {
           *reinterpret_cast<double2*>(wrow) = make_double2(v0, v1);
           out(j0 + rw, c0, v0);
@@ -156,18 +171,19 @@ __device__ void blk_sweep(const BlkCtx& cx, int& chunk, int n, int kw, int strid
       for (int t = warp; t < 2 * tiles; t += 8) {
         const int rt = t >> 1, nh = t & 1;
         const int r0 = rt * 8 + g;  // below-row of this lane's A / C fragments
-        double* crow = win + ((j0 + BK + r0) % W) * BSR + nh * 8 + 2 * q;
-        double acc[2] = {crow[0], crow[1]};
+        double* crow = win + wr(BK + r0) * BSR + nh * 8 + 2 * q;
+        double acc[2] = {0.0, 0.0};  // L[below, block] X[block], subtracted once
 #pragma unroll
         for (int k0 = 0; k0 < BK; k0 += 4) {
           const int s = k0 + q;
           const int tt = BK + r0 - s;  // row offset from step s (>= 1)
-          const double a = (s < nb && tt <= kw) ? -rec(s)[tt - 1] : 0.0;
-          const double b = win[((j0 + k0 + q) % W) * BSR + nh * 8 + g];
+          const double* rs = (k0 < BCH ? rec0 + s * stride : rec1 + (s - BCH) * stride);
+          const double a = (s < nb && tt <= kw) ? rs[tt - 1] : 0.0;
+          const double b = win[wr(k0 + q) * BSR + nh * 8 + g];
           dmma_b(acc, a, b);
         }
-        crow[0] = acc[0];
-        crow[1] = acc[1];
+        crow[0] -= acc[0];
+        crow[1] -= acc[1];
       }
       csync();
       tb += clock64() - c2t;
@@ -178,8 +194,8 @@ __device__ void blk_sweep(const BlkCtx& cx, int& chunk, int n, int kw, int strid
         const double* r = rec(s);
         const int p = __double2int_rn(r[kw]);
         if (p != j && tid < 16) {
-          double* a = win + (j % W) * BSR + tid;
-          double* b = win + (p % W) * BSR + tid;
+          double* a = win + wr(s) * BSR + tid;
+          double* b = win + wr(p - j0) * BSR + tid;
           const double tmp = *a;
           *a = *b;
           *b = tmp;
@@ -187,14 +203,14 @@ __device__ void blk_sweep(const BlkCtx& cx, int& chunk, int n, int kw, int strid
         csync();
         for (int e = tid; e < kw * 16; e += 256) {
           const int t = (e >> 4) + 1, c = e & 15;
-          double* dst = win + ((j + t) % W) * BSR + c;
-          *dst = fma(-r[t - 1], win[(j % W) * BSR + c], *dst);
+          double* dst = win + wr(s + t) * BSR + c;
+          *dst = fma(-r[t - 1], win[wr(s) * BSR + c], *dst);
         }
         csync();
       }
       for (int e = tid; e < nb * 16; e += 256) {
         const int Rw = e >> 4, c = e & 15;
-        out(j0 + Rw, c, win[((j0 + Rw) % W) * BSR + c]);
+        out(j0 + Rw, c, win[wr(Rw) * BSR + c]);
       }
     }
     csync();  // records and the block's rows consumed
@@ -206,7 +222,7 @@ __device__ void blk_sweep(const BlkCtx& cx, int& chunk, int n, int kw, int strid
 #pragma unroll
     for (int q2 = 0; q2 < 2; ++q2) {
       const int e = tid + 256 * q2, i = e >> 4, c = e & 15;
-      if (i < nb) win[((j0 + i) % W) * BSR + c] = nxt[q2];
+      if (i < nb) win[wr(i) * BSR + c] = nxt[q2];
     }
     csync();
     tr += clock64() - c0t;
