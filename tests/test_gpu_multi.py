@@ -6,6 +6,8 @@ cheap, against the CPU oracle / the reference's golden values directly.
 Bars: apply columns rel <= 1e-12 vs the single apply (1e-10 vs the reference),
 SpMM bitwise, GMRES iterations +-1 and solution rel <= 1e-8 per column."""
 
+import os
+
 import numpy as np
 import pytest
 import scipy.sparse as sp
@@ -91,7 +93,10 @@ def test_apply_multi_one_level(cfg1):
     got = pre1.apply_multi(R)
     assert rel(got[:, 1], g["apply_one_level_r"]) <= APPLY_RTOL
     want = np.stack([pre1.apply(R[:, c]) for c in range(5)], axis=1)
-    assert np.array_equal(got, want)  # no coarse part: same kernels, same order, bitwise
+    if os.environ.get("HG_LOCAL_BLOCKED", "0") == "1":  # blocked solve: DMMA band updates, different rounding
+        assert colrel(got, want) <= 1e-12
+    else:
+        assert np.array_equal(got, want)  # no coarse part: same per-column arithmetic, bitwise
 
 
 def test_apply_multi_unpremultiplied_coarse_tiles(cfg1, monkeypatch):
