@@ -250,6 +250,33 @@ def read_stats(lib):
     return dict(zip(_lib.PHASES, ms.tolist())), dict(zip(_lib.PHASES, cnt.tolist()))
 
 
+def build_shared(args, dist):
+    """The host setup once per job: rank 0 builds the problem, the other ranks
+    load its pickle (N ranks would otherwise redo the ~1 min host setup side
+    by side on the same host cores)."""
+    import pickle
+
+    import paper_2406_06283_b200 as hg
+
+    if dist.world == 1:
+        return hg.build_problem(args.config, cstab=args.cstab, verbose=True)
+    path = os.path.join(tempfile.gettempdir(), "hg_setup_%s_%s_%s.pkl" % (
+        args.config, os.environ.get("MASTER_PORT", "0"), os.environ.get("TORCHELASTIC_RUN_ID", "run")))
+    if dist.rank == 0:
+        P = hg.build_problem(args.config, cstab=args.cstab, verbose=True)
+        with open(path + ".tmp", "wb") as fh:
+            pickle.dump(P, fh, protocol=pickle.HIGHEST_PROTOCOL)
+        os.replace(path + ".tmp", path)
+    dist.barrier()
+    if dist.rank != 0:
+        with open(path, "rb") as fh:
+            P = pickle.load(fh)
+    dist.barrier()
+    if dist.rank == 0:
+        os.unlink(path)
+    return P
+
+
 def run_ours(args, dist):
     import torch
 
@@ -259,7 +286,7 @@ def run_ours(args, dist):
     torch.cuda.set_device(dist.local)
     lib = _lib.load()
     t0 = time.perf_counter()
-    P = hg.build_problem(args.config, cstab=args.cstab, verbose=dist.rank == 0)
+    P = build_shared(args, dist)
     t_setup = time.perf_counter() - t0
     t0 = time.perf_counter()
     pre = hg.factorize(P.forms, P.dec, P.coarse)
