@@ -51,6 +51,7 @@ __device__ __forceinline__ void dmma_b(double (&d)[2], double a, double b) {
 }
 
 struct BlkCtx {
+  double2* bcast;      // [8 warps][2] step-row broadcast slots
   double* win;         // [wrows][BSR]
   int wrows;
   const double* ring;
@@ -59,13 +60,21 @@ struct BlkCtx {
   int stage_stride;
 };
 
-// one chain step s of a block for this lane's row rw and its warp's two columns
+// one chain step s of a block for this lane's row rw and its warp's two
+// columns; the step row's values reach the warp through a shared-memory slot
+// (one 16-byte store by lane s, one broadcast load) instead of four shuffles
 template <bool FWD>
 __device__ __forceinline__ void blk_step(int s, const double* __restrict__ r, int rw, int kw, double& v0,
-                                         double& v1) {
+                                         double& v1, double2* slot) {
   const bool below = rw > s && rw - s <= kw;
   const double m = below ? r[rw - s - 1] : 0.0;
-  double x0 = __shfl_sync(FULL, v0, s), x1 = __shfl_sync(FULL, v1, s);
+  // double-buffered by step parity: one warp barrier per step (a lane cannot
+  // rewrite slot[s & 1] before every lane passed step s+1's barrier)
+  double2* sl = slot + (s & 1);
+  if (rw == s) *sl = make_double2(v0, v1);
+  __syncwarp();
+  const double2 xs2 = *sl;
+  double x0 = xs2.x, x1 = xs2.y;
   if (!FWD) {
     const double dv = r[kw];
     x0 *= dv;
@@ -145,6 +154,7 @@ __device__ void blk_sweep(const BlkCtx& cx, int& chunk, int n, int kw, int strid
       {
         const int rw = lane;  // block row of this lane
         const int c0 = 2 * warp;
+        double2* bslot = cx.bcast + 2 * warp;
         double* wrow = win + wr(rw) * BSR + c0;
         const double2 t2 = *reinterpret_cast<const double2*>(wrow);
         double v0 = t2.x, v1 = t2.y;
@@ -152,10 +162,10 @@ __device__ void blk_sweep(const BlkCtx& cx, int& chunk, int n, int kw, int strid
         const int n0 = min(nb, BCH);
         const double* r = rec0;
 #pragma unroll 4
-        for (int s = 0; s < n0; ++s, r += stride) blk_step<FWD>(s, r, rw, kw, v0, v1);
+        for (int s = 0; s < n0; ++s, r += stride) blk_step<FWD>(s, r, rw, kw, v0, v1, bslot);
         r = rec1;
 #pragma unroll 4
-        for (int s = BCH; s < nb; ++s, r += stride) blk_step<FWD>(s, r, rw, kw, v0, v1);
+        for (int s = BCH; s < nb; ++s, r += stride) blk_step<FWD>(s, r, rw, kw, v0, v1, bslot);
         if (rw < nb) {
           *reinterpret_cast<double2*>(wrow) = make_double2(v0, v1);
           out(j0 + rw, c0, v0);
@@ -273,7 +283,8 @@ __global__ void __launch_bounds__(BTHREADS, 2) k_local_blocked(const LocalDesc* 
   }
   // named barrier 0 is used by __syncthreads: the producer warp has returned,
   // so the consumers synchronise among themselves with bar.sync 1, 256
-  BlkCtx cx{sm + (size_t)BNS * stage_stride, wrows, sm, full, empty, stage_stride};
+  __shared__ double2 bcast[16];
+  BlkCtx cx{bcast, sm + (size_t)BNS * stage_stride, wrows, sm, full, empty, stage_stride};
   int chunk = 0;
   blk_sweep<true>(cx, chunk, d.n, d.kl, d.fstride, idx + d.idx_off, R, ldr, xs + d.idx_off, xs_len, nrhs);
   blk_sweep<false>(cx, chunk, d.n, d.kv, d.bstride, nullptr, nullptr, 0, xs + d.idx_off, xs_len, nrhs);
