@@ -433,35 +433,48 @@ int launch_b0_multi(HgPrecond* P, int nrhs, cudaStream_t st, unsigned long long 
 }
 
 // ------------------------------------------------------------------ assembly
+// one thread per dof, all columns: the contributor lists are read once (not
+// once per column); per column the sum runs in the reference's fixed order
 __global__ void __launch_bounds__(256) k_assemble_multi(int n, const int* __restrict__ cptr,
                                                         const long long* __restrict__ cent,
                                                         const double* __restrict__ zsm, long long zs_len,
                                                         const int* __restrict__ lptr,
                                                         const long long* __restrict__ lent,
                                                         const double* __restrict__ xsm, long long xs_len,
-                                                        double* __restrict__ out, long long ldo) {
+                                                        double* __restrict__ out, long long ldo, int nrhs) {
   const int d = blockIdx.x * 256 + threadIdx.x;
-  const int c = blockIdx.y;
   if (d >= n) return;
-  double acc = 0.0;
+  double acc[MR];
+#pragma unroll
+  for (int c = 0; c < MR; ++c) acc[c] = 0.0;
   if (cptr) {
-    const double* z = zsm + (long long)c * zs_len;
-    for (int e = cptr[d]; e < cptr[d + 1]; ++e) acc += z[cent[e]];
+    for (int e = cptr[d]; e < cptr[d + 1]; ++e) {
+      const double* z = zsm + cent[e];
+#pragma unroll
+      for (int c = 0; c < MR; ++c)
+        if (c < nrhs) acc[c] += z[(long long)c * zs_len];
+    }
   }
   if (lptr) {
-    const double* x = xsm + (long long)c * xs_len;
-    for (int e = lptr[d]; e < lptr[d + 1]; ++e) acc += x[lent[e]];
+    for (int e = lptr[d]; e < lptr[d + 1]; ++e) {
+      const double* x = xsm + lent[e];
+#pragma unroll
+      for (int c = 0; c < MR; ++c)
+        if (c < nrhs) acc[c] += x[(long long)c * xs_len];
+    }
   }
-  out[(long long)c * ldo + d] = acc;
+#pragma unroll
+  for (int c = 0; c < MR; ++c)
+    if (c < nrhs) out[(long long)c * ldo + d] = acc[c];
 }
 
 int launch_assemble_multi(HgPrecond* P, bool with_coarse, bool with_local, double* OUT, long long ldo, int nrhs,
                           cudaStream_t st) {
   if (P->n == 0 || nrhs == 0) return HG_OK;
   const bool coarse = with_coarse && P->m > 0;
-  k_assemble_multi<<<dim3(ceil_div(P->n, 256), nrhs), 256, 0, st>>>(
-      P->n, coarse ? P->d_cptr : nullptr, P->d_cent, P->d_zsm, P->zs_len, with_local ? P->d_lptr : nullptr,
-      P->d_lent, P->d_xsm, P->xs_len, OUT, ldo);
+  k_assemble_multi<<<ceil_div(P->n, 256), 256, 0, st>>>(P->n, coarse ? P->d_cptr : nullptr, P->d_cent, P->d_zsm,
+                                                        P->zs_len, with_local ? P->d_lptr : nullptr, P->d_lent,
+                                                        P->d_xsm, P->xs_len, OUT, ldo, nrhs);
   HG_LAUNCH_CHECK();
   return HG_OK;
 }
