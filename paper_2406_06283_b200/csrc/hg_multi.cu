@@ -787,7 +787,7 @@ int launch_dots2_batch(int n, const double* A, long long lda, const double* U, l
 //   q  = (V_c[j] - sum_{i<j} s_i V_c[i]) * rinv          (q_j re-orthogonalised)
 //   w  = w * rinv - sum_{i<j} c_i V_c[i] - c_j q          (w projected)
 // coef row of column c: [rinv, s_0..s_{j-1}, c_0..c_j].
-__global__ void __launch_bounds__(VEC_THREADS, 3) k_dcgs2_update(int n, double* __restrict__ V, long long ldv,
+__global__ void __launch_bounds__(VEC_THREADS, 4) k_dcgs2_update(int n, double* __restrict__ V, long long ldv,
                                                               long long ldcol, int j, double* __restrict__ w,
                                                               long long ldw, const double* __restrict__ coef,
                                                               long long ldcoef, ColList cols) {
