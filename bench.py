@@ -262,17 +262,29 @@ def build_shared(args, dist):
         return hg.build_problem(args.config, cstab=args.cstab, verbose=True)
     path = os.path.join(tempfile.gettempdir(), "hg_setup_%s_%s_%s.pkl" % (
         args.config, os.environ.get("MASTER_PORT", "0"), os.environ.get("TORCHELASTIC_RUN_ID", "run")))
+    P, ok = None, 0.0
     if dist.rank == 0:
         P = hg.build_problem(args.config, cstab=args.cstab, verbose=True)
-        with open(path + ".tmp", "wb") as fh:
-            pickle.dump(P, fh, protocol=pickle.HIGHEST_PROTOCOL)
-        os.replace(path + ".tmp", path)
-    dist.barrier()
+        try:
+            with open(path + ".tmp", "wb") as fh:
+                pickle.dump(P, fh, protocol=pickle.HIGHEST_PROTOCOL)
+            os.replace(path + ".tmp", path)
+            ok = 1.0
+        except OSError as exc:  # no room for the pickle: every rank builds its own
+            log("shared setup unavailable (%s); each rank builds the problem" % exc)
+            try:
+                os.unlink(path + ".tmp")
+            except OSError:
+                pass
+    ok = dist.max(ok)  # rank 0's verdict (the others contribute 0)
     if dist.rank != 0:
-        with open(path, "rb") as fh:
-            P = pickle.load(fh)
+        if ok:
+            with open(path, "rb") as fh:
+                P = pickle.load(fh)
+        else:
+            P = hg.build_problem(args.config, cstab=args.cstab, verbose=False)
     dist.barrier()
-    if dist.rank == 0:
+    if dist.rank == 0 and ok:
         os.unlink(path)
     return P
 
