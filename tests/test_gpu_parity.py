@@ -235,3 +235,33 @@ def test_config_parity_vs_oracle(name, orth):
     assert rep.converged and info["converged"]
     assert abs(rep.iterations - info["iterations"]) <= 1
     assert rel(x, xo) <= SOL_RTOL
+
+
+def _small_pipeline(n, M, q, k):
+    mesh = hg.build_unit_square_mesh(n)
+    space = hg.build_fe_space(mesh)
+    forms = hg.assemble_forms(mesh, space, hg.coefficient_field(mesh), k)
+    return forms, hg.build_two_level(mesh, space, M, q)
+
+
+def test_spd_flags_for_small_k():
+    """test_schwarz.py:118-124 on the device factorisation."""
+    forms, dec = _small_pipeline(8, 2, 2, 1.0)
+    pre = hg.factorize(forms, dec, None)
+    assert all(ls.spd_flag for ls in pre.local_solvers)
+    assert all(ls.min_eig > 0 for ls in pre.local_solvers)
+
+
+def test_factorization_consistency_device_solves():
+    """test_schwarz.py:127-138 through the device local solves (ls.lu.solve)."""
+    forms, dec = _small_pipeline(8, 2, 2, 5.0)
+    pre = hg.factorize(forms, dec, None)
+    B = forms.helmholtz.tocsr()
+    rng = np.random.default_rng(10)
+    for ls in pre.local_solvers:
+        block = B[ls.idof][:, ls.idof]
+        x = rng.standard_normal(ls.idof.size)
+        back = ls.lu.solve(np.asarray(block @ x))
+        assert np.abs(back - np.asarray(block @ ls.lu.solve(x))).max() <= 1e-9
+        y = ls.lu.solve(x)
+        assert np.abs(np.asarray(block @ y) - x).max() <= 1e-10 * np.abs(x).max()
