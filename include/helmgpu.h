@@ -255,6 +255,12 @@ int hg_gmres_batch(HgOp* op, HgOp* weight, const double* rhs, int64_t ldr, doubl
 int hg_set_orthogonalization(int mode);
 int hg_get_orthogonalization(void);
 
+/* Krylov basis of the last hg_gmres / hg_gmres_batch solve on `op`
+ * (inspection hook, mirrors test_wgmres.py:35-52): copies basis vectors
+ * 0..nv-1 of column `col` into out (device, nv x n, vector i at out + i*n).
+ * nv must not exceed the vectors the solve produced (its iterations). */
+int hg_op_basis(HgOp* op, int32_t col, int32_t nv, double* out, void* stream);
+
 /* Phase timing of hg_gmres / hg_gmres_batch (measurement hook, used by
  * bench.py to time kernels live inside its timed region).  While enabled,
  * each phase of each iteration is bracketed by CUDA events on the solve's

@@ -110,6 +110,7 @@ SIGNATURES = {
         [_vp, _f64p, _f64p, ctypes.c_int32, ctypes.c_double, ctypes.c_int32, _f64p, _i32p, _vp],
     ),
     "hg_stats_enable": (ctypes.c_int, [ctypes.c_int]),
+    "hg_op_basis": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp]),
     "hg_set_orthogonalization": (ctypes.c_int, [ctypes.c_int]),
     "hg_get_orthogonalization": (ctypes.c_int, []),
     "hg_stats_read": (ctypes.c_int, [_f64p, _i64p, ctypes.c_int]),

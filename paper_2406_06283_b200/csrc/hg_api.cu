@@ -309,6 +309,10 @@ struct HgOp {
   BatchWs bws;
   DcWs dws;    // one right-hand side
   DcWs dwsb;   // batches
+  // basis of the last solve (hg_op_basis): vector i of column c at base + c*ldcol + i*ldv
+  const double* basis = nullptr;
+  long long basis_ldv = 0, basis_ldcol = 0;
+  int basis_cols = 0, basis_nv = 0;
 };
 
 // Orthogonalisation scheme of hg_gmres / hg_gmres_batch (hg_set_orthogonalization).
@@ -1259,6 +1263,11 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
   }
   HG_CUDA_TRY(cudaStreamSynchronize(st));
   stats_collect();
+  op->basis = V;
+  op->basis_ldv = ld;
+  op->basis_ldcol = 0;
+  op->basis_cols = 1;
+  op->basis_nv = m;
   info[0] = m;
   info[1] = converged ? 1 : 0;
   info[2] = breakdown ? 1 : 0;
@@ -1641,6 +1650,12 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
   }
   HG_CUDA_TRY(cudaStreamSynchronize(st));
   stats_collect();
+  op->basis = Q;
+  op->basis_ldv = vstride;
+  op->basis_ldcol = n;
+  op->basis_cols = nrhs;
+  op->basis_nv = 0;
+  for (int c = 0; c < nrhs; ++c) op->basis_nv = std::max(op->basis_nv, mlist[c]);
   if (host_timing()) {
     const double tot = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
     fprintf(stderr, "[dcgs2 host] nrhs %d: total %.1f ms, waiting at the per-iteration sync %.1f ms, host work "
@@ -1931,6 +1946,12 @@ extern "C" int hg_gmres_batch(HgOp* op, HgOp* weight, const double* rhs, int64_t
   }
   HG_CUDA_TRY(cudaStreamSynchronize(st));
   stats_collect();
+  op->basis = V;
+  op->basis_ldv = vstride;
+  op->basis_ldcol = n;
+  op->basis_cols = nrhs;
+  op->basis_nv = 0;
+  for (int c = 0; c < nrhs; ++c) op->basis_nv = std::max(op->basis_nv, mlist[c]);
   for (int c = 0; c < nrhs; ++c) {
     info[4 * c] = mlist[c];
     info[4 * c + 1] = cst[c].converged ? 1 : 0;
@@ -1965,4 +1986,18 @@ extern "C" int hg_solve_host_batch(HgPrecond* P, const double* F_host, double* X
   cudaFreeAsync(d_x, st);
   HG_CUDA_TRY(cudaStreamSynchronize(st));
   return s;
+}
+
+extern "C" int hg_op_basis(HgOp* op, int32_t col, int32_t nv, double* out, void* stream) {
+  if (!op || !out || !op->basis || col < 0 || col >= op->basis_cols || nv < 0 || nv > op->basis_nv) {
+    set_error("hg_op_basis: no such basis (solve first; col / nv out of range)");
+    return HG_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t vb = sizeof(double) * (size_t)op->n;
+  if (nv > 0)
+    HG_CUDA_TRY(cudaMemcpy2DAsync(out, vb, op->basis + (long long)col * op->basis_ldcol, sizeof(double) * op->basis_ldv,
+                                  vb, nv, cudaMemcpyDeviceToDevice, st));
+  HG_CUDA_TRY(cudaStreamSynchronize(st));
+  return HG_OK;
 }

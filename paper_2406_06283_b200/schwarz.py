@@ -551,6 +551,11 @@ class DeviceOperator:
         _lib.check(_lib.load().hg_op_apply(self._handle, _vp(t), _vp(out), _stream()), "hg_op_apply")
         return out.cpu().numpy() if was_np else out
 
+    def basis(self, nv, col=0):
+        """The first nv Krylov basis vectors of column col of the last GMRES
+        solve on this operator, as an (nv, n) CUDA tensor (inspection hook)."""
+        return _basis(self._handle, self.n, col, nv)
+
     def apply_multi(self, V):
         """op applied to every column of a batch (numpy (n, nrhs) or CUDA (nrhs, n))."""
         torch = _torch()
@@ -569,6 +574,13 @@ class DeviceOperator:
                 self._handle = None
         except Exception:
             pass
+
+
+def _basis(handle, n, col, nv):
+    torch = _torch()
+    out = torch.empty((nv, n), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.load().hg_op_basis(handle, int(col), int(nv), _vp(out), _stream()), "hg_op_basis")
+    return out
 
 
 class CsrOperator:
@@ -601,6 +613,11 @@ class CsrOperator:
         out = torch.empty_like(t)
         _lib.check(_lib.load().hg_op_apply(self._handle, _vp(t), _vp(out), _stream()), "hg_op_apply")
         return out.cpu().numpy() if was_np else out
+
+    def basis(self, nv, col=0):
+        """The first nv Krylov basis vectors of column col of the last GMRES
+        solve on this operator, as an (nv, n) CUDA tensor (inspection hook)."""
+        return _basis(self._handle, self.n, col, nv)
 
     def apply_multi(self, V):
         """op applied to every column of a batch (numpy (n, nrhs) or CUDA (nrhs, n))."""

@@ -265,3 +265,26 @@ def test_factorization_consistency_device_solves():
         assert np.abs(back - np.asarray(block @ ls.lu.solve(x))).max() <= 1e-9
         y = ls.lu.solve(x)
         assert np.abs(np.asarray(block @ y) - x).max() <= 1e-10 * np.abs(x).max()
+
+
+@pytest.mark.parametrize("orth", ORTHS)
+def test_weighted_basis_orthonormality(orth):
+    """test_wgmres.py:35-52: the Krylov basis is W-orthonormal to 1e-10 over
+    50 iterations (basis read back through hg_op_basis)."""
+    rng = np.random.default_rng(2)
+    n = 60
+    A = rng.standard_normal((n, n)) + n * np.eye(n)  # the reference's _random_system
+    b = rng.standard_normal(n)
+    G = rng.standard_normal((n, n))
+    W = sp.csr_matrix(G @ G.T + n * np.eye(n))
+    op = hg.CsrOperator(A)
+    x, rep = hg.weighted_gmres(op, b, weight=W, rtol=0.0, maxit=50, orth=orth)
+    assert rep.iterations == 50
+    V = op.basis(50).cpu().numpy().T
+    gram = V.T @ (W @ V)
+    assert np.abs(gram - np.eye(50)).max() <= 1e-10
+    B = np.stack([b, rng.standard_normal(n)], axis=1)
+    X, reps = hg.weighted_gmres_batch(op, B, weight=W, rtol=0.0, maxit=40, orth=orth)
+    for c in range(2):
+        Vc = op.basis(40, col=c).cpu().numpy().T
+        assert np.abs(Vc.T @ (W @ Vc) - np.eye(40)).max() <= 1e-10
