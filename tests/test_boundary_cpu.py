@@ -54,3 +54,35 @@ def test_python_constants_match_header():
     assert int(consts["HG_ABI_VERSION"]) == _lib.ABI_VERSION
     assert int(consts["HG_ORTH_MEASURED"]) == _lib.ORTH["measured"]
     assert int(consts["HG_ORTH_DCGS2"]) == _lib.ORTH["dcgs2"]
+
+
+def test_elman_gamma_conventions():
+    """test_wgmres.py:112-126 on the mirror's host helper (no device needed)."""
+    from paper_2406_06283_b200 import elman_gamma
+
+    assert elman_gamma(1.0, 1.0, c2_bounds="norm") == 1.0
+    assert elman_gamma(1.0, 4.0, c2_bounds="norm") == 0.25
+    assert elman_gamma(1.0, 4.0) == 0.5
+    s, lam, theta = 0.5, 1.0, 0.01
+    c1 = (1 - s) / (2 + 3 * lam**4 * theta)
+    c2 = 18.0 + 8.0 * lam**3
+    assert c1 == pytest.approx(0.24630541871921183, rel=1e-12) and c2 == 26.0
+    assert elman_gamma(c1, c2, c2_bounds="norm") == pytest.approx(c1 / 26.0)
+    with pytest.raises(ValueError):
+        elman_gamma(-1.0, 2.0)
+    with pytest.raises(ValueError):
+        elman_gamma(1.0, 2.0, c2_bounds="bogus")
+
+
+def test_envelope_fields_host():
+    """The envelope part of test_wgmres.py:96-109 (wgmres._envelope)."""
+    import numpy as np
+
+    from paper_2406_06283_b200.wgmres import _envelope
+
+    env, clamped = _envelope(0.5, 3.0, 4)
+    assert env.size == 5 and env[0] == 3.0 and not clamped
+    assert env[1] / env[0] == pytest.approx(np.sqrt(1 - 0.25))
+    env, clamped = _envelope(1.0, 3.0, 4)
+    assert clamped and np.all(env[1:] == 0.0)
+    assert _envelope(None, 3.0, 4) == (None, False)
