@@ -704,9 +704,14 @@ __global__ void __launch_bounds__(VEC_THREADS, 3) k_dots2_batch(int n, const dou
                                                              const double* __restrict__ U, long long ldu,
                                                              const double* __restrict__ V, long long ldv,
                                                              long long ldcol, int nv, ColList cols,
-                                                             double* __restrict__ partials, int width, int nb) {
+                                                             double* __restrict__ partials, int width, int nb,
+                                                             int vsplit) {
   __shared__ double s_p[2][VEC_THREADS / 32][2 * D2_CH];
-  const int c = cols.c[blockIdx.y];
+  const int c = cols.c[blockIdx.y / vsplit];
+  // basis vectors [ia, ib) of this block (vsplit blocks share a row tile when
+  // the grid would otherwise be a few waves of one column)
+  const int per = ((nv + vsplit - 1) / vsplit + D2_CH - 1) / D2_CH * D2_CH;
+  const int ia = (blockIdx.y % vsplit) * per, ib = min(nv, ia + per);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double av[VEC_ROWS], uv[VEC_ROWS];
   int rows[VEC_ROWS];
@@ -721,13 +726,13 @@ __global__ void __launch_bounds__(VEC_THREADS, 3) k_dots2_batch(int n, const dou
   double* pc = partials + (long long)c * width * nb;
   const int my = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
   int buf = 0;
-  for (int i0 = 0; i0 < nv; i0 += D2_CH, buf ^= 1) {
+  for (int i0 = ia; i0 < ib; i0 += D2_CH, buf ^= 1) {
     double x[D2_CH][VEC_ROWS];
 #pragma unroll
     for (int t = 0; t < D2_CH; ++t)
 #pragma unroll
       for (int k = 0; k < VEC_ROWS; ++k)
-        x[t][k] = (i0 + t < nv && rows[k] >= 0) ? __ldg(Vc + (long long)(i0 + t) * ldv + rows[k]) : 0.0;
+        x[t][k] = (i0 + t < ib && rows[k] >= 0) ? __ldg(Vc + (long long)(i0 + t) * ldv + rows[k]) : 0.0;
     double v[2 * D2_CH];
 #pragma unroll
     for (int t = 0; t < D2_CH; ++t) {
@@ -748,7 +753,7 @@ __global__ void __launch_bounds__(VEC_THREADS, 3) k_dots2_batch(int n, const dou
       double sum = 0.0;
 #pragma unroll
       for (int w = 0; w < VEC_THREADS / 32; ++w) sum += s_p[buf][w][threadIdx.x];
-      if (i0 + t < nv) pc[(long long)(which * nv + i0 + t) * nb + blockIdx.x] = sum;
+      if (i0 + t < ib) pc[(long long)(which * nv + i0 + t) * nb + blockIdx.x] = sum;
     }
   }
 }
@@ -775,8 +780,10 @@ int launch_dots2_batch(int n, const double* A, long long lda, const double* U, l
                        long long ow, cudaStream_t st) {
   const int nb = ceil_div(n, VEC_TILE);
   if (n == 0 || cols.n == 0) return HG_OK;
-  k_dots2_batch<<<dim3(nb, cols.n), VEC_THREADS, 0, st>>>(n, A, lda, U, ldu, V, ldv, ldcol, nv, cols, partials,
-                                                          2 * nv, nb);
+  // few columns: split the basis over blocks so the grid is many waves deep
+  const int vsplit = (cols.n * nb < 4096 && nv >= 4 * D2_CH) ? 2 : 1;
+  k_dots2_batch<<<dim3(nb, cols.n * vsplit), VEC_THREADS, 0, st>>>(n, A, lda, U, ldu, V, ldv, ldcol, nv, cols,
+                                                                   partials, 2 * nv, nb, vsplit);
   HG_LAUNCH_CHECK();
   k_reduce_vm<<<dim3(2 * nv, cols.n), 256, 0, st>>>(partials, nb, 2 * nv, cols, out, ow);
   HG_LAUNCH_CHECK();
