@@ -61,7 +61,7 @@ extern "C" {
 #define HG_ERR_UNSUPPORTED 3
 #define HG_ERR_NOMEM 4
 
-#define HG_ABI_VERSION 2
+#define HG_ABI_VERSION 3
 
 /* Most right-hand sides one batched call handles (BASELINE config 5's
  * batch of 16 seeded load vectors). */
@@ -172,6 +172,14 @@ int hg_shutdown(void);
 
 /* ---- preconditioner (schwarz.factorize / TwoLevelPreconditioner) ---- */
 int hg_precond_create(const HgPrecondDesc* desc, HgPrecond** out);
+/* Fault state of a handle (no synchronisation).  The coarse solve is
+ * launched on a side stream ahead of the Z^T r it consumes and waits for it
+ * on the device; every such wait is bounded (default 10 s, hg_debug_set).  A
+ * timed-out wait, or a launch that fails part-way through an apply, poisons
+ * the handle: this and every later call on it return HG_ERR_CUDA with a
+ * message (destroy and recreate it).  The reference's apply never raises
+ * (SPEC.md:359); a device fault is the one exception. */
+int hg_precond_status(HgPrecond* p);
 int hg_precond_destroy(HgPrecond* p);
 /* device bytes held by the handle */
 int64_t hg_precond_device_bytes(const HgPrecond* p);
@@ -214,6 +222,13 @@ int hg_op_create_csr(int32_t n, int64_t nnz, const int32_t* indptr, const int32_
  * The operator borrows the handle (destroy the op first). */
 int hg_op_create_precond(HgPrecond* p, int mode, HgOp** out);
 int hg_op_destroy(HgOp* op);
+/* Release the operator's Krylov bases and GMRES workspaces (the op stays
+ * usable; the next solve maps them again).  hg_op_basis is unavailable until
+ * then.  Memory plan: a solve whose worst-case basis (nrhs (maxit+1) n
+ * doubles) does not fit the free device memory first releases the idle
+ * bases of the other ops of the process, then solves its batch in
+ * sub-batches of columns. */
+int hg_op_release(HgOp* op);
 int hg_op_apply(HgOp* op, const double* x, double* y, void* stream);
 /* Y[:, c] = op(X[:, c]), c < nrhs (batched SpMM / batched apply). */
 int hg_op_apply_multi(HgOp* op, const double* X, int64_t ldx, double* Y, int64_t ldy, int32_t nrhs, void* stream);
@@ -235,7 +250,9 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
  * history: host, nrhs * (maxit+1) doubles (column c at c*(maxit+1));
  * info: host, nrhs * 4 ints (as hg_gmres, column c at 4c).  The Krylov
  * bases live in a virtual reservation that is backed by device memory only
- * as far as the iterations actually reach. */
+ * as far as the iterations actually reach.  maxit is capped at 1024 (the
+ * basis kernels keep their coefficients in shared memory): a larger
+ * min(maxit, n) returns HG_ERR_UNSUPPORTED before any work (hg_gmres too). */
 int hg_gmres_batch(HgOp* op, HgOp* weight, const double* rhs, int64_t ldr, double* x, int64_t ldx, int32_t nrhs,
                    double rtol, int32_t maxit, double* history, int32_t* info, void* stream);
 
@@ -252,8 +269,27 @@ int hg_gmres_batch(HgOp* op, HgOp* weight, const double* rhs, int64_t ldr, doubl
  *   +-1, solution 1e-8) are tested against the reference for both modes. */
 #define HG_ORTH_MEASURED 0
 #define HG_ORTH_DCGS2 1
+/* per host thread (the bindings set it around one call) */
 int hg_set_orthogonalization(int mode);
 int hg_get_orthogonalization(void);
+/* DCGS2 safety: when rho^2 = a_j - s.s <= 1e-8 a_j (cancellation: q_j
+ * nearly in span Q), that column takes an explicit pass instead (q_j -= Q s
+ * on the device, rho measured as ||q_j||_W directly).  Process-wide count of
+ * such passes; each also counts in the column's info[3]. */
+int64_t hg_dcgs2_explicit_passes(void);
+
+/* Test hooks (no reference analogue).  Keys:
+ *   HG_DEBUG_SPIN_LIMIT_MS     process-wide bound of device-side waits, ms
+ *                              (0 = unbounded; default 10000)
+ *   HG_DEBUG_SKIP_ZT           drop the next `value` Z^T r launches of handle
+ *                              p (fault injection: the paired coarse solve
+ *                              must time out and poison p, not hang)
+ *   HG_DEBUG_FORCE_EXPLICIT_RHO  DCGS2 takes the explicit rho pass on every
+ *                              column and iteration (value != 0) */
+#define HG_DEBUG_SPIN_LIMIT_MS 1
+#define HG_DEBUG_SKIP_ZT 2
+#define HG_DEBUG_FORCE_EXPLICIT_RHO 3
+int hg_debug_set(HgPrecond* p, int32_t key, int64_t value);
 
 /* Krylov basis of the last hg_gmres / hg_gmres_batch solve on `op`
  * (inspection hook, mirrors test_wgmres.py:35-52): copies basis vectors

@@ -114,9 +114,15 @@ SIGNATURES = {
     "hg_set_orthogonalization": (ctypes.c_int, [ctypes.c_int]),
     "hg_get_orthogonalization": (ctypes.c_int, []),
     "hg_stats_read": (ctypes.c_int, [_f64p, _i64p, ctypes.c_int]),
+    "hg_precond_status": (ctypes.c_int, [_vp]),
+    "hg_op_release": (ctypes.c_int, [_vp]),
+    "hg_dcgs2_explicit_passes": (ctypes.c_int64, []),
+    "hg_debug_set": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int64]),
 }
 
-ABI_VERSION = 2
+ABI_VERSION = 3
+DEBUG_SPIN_LIMIT_MS, DEBUG_SKIP_ZT, DEBUG_FORCE_EXPLICIT_RHO = 1, 2, 3
+MAX_BASIS = 1024  # Krylov vectors the basis kernels support (MAX_NV)
 NPHASES = 7  # HG_NPHASES
 ORTH = {"measured": 0, "dcgs2": 1}
 PHASES = ("op_apply", "proj_dots", "cgs_update", "measure", "second_pass", "append", "w_spmv")

@@ -290,7 +290,10 @@ def solve_gevp_lanczos(gevp, n_wanted, shift=None, tol=0.0, ncv=None):
             mu, U = mu[order], U[:, order]
         else:
             nc = ncv or min(nI, max(2 * k_ask + 1, k_ask + 40))
-            mu, U = spla.eigsh(op, k=k_ask, which="LM", tol=tol, ncv=nc, maxiter=100 * nI)
+            # seeded start vector: ARPACK's own default draws from a per-process
+            # stream, so results would depend on which pool worker ran which block
+            v0 = np.random.default_rng(7919 + gevp.subdomain_index).standard_normal(nI)
+            mu, U = spla.eigsh(op, k=k_ask, which="LM", tol=tol, ncv=nc, maxiter=100 * nI, v0=v0)
         if np.any(mu < 0.0):
             # an eigenvalue below -g: widen the shift so the lowest ones are positive
             lam_neg = 1.0 / mu[mu < 0.0] - g

@@ -13,6 +13,10 @@
 
 #include <cuda.h>
 
+#include <map>
+#include <mutex>
+#include <set>
+
 #include "hg_internal.cuh"
 
 namespace hg {
@@ -22,6 +26,35 @@ static std::atomic<long long> g_launches{0};
 
 void set_error(const std::string& msg) { g_err = msg; }
 void count_launch(int n) { g_launches += n; }
+
+// ---- bounded waits and fault injection (hg_debug_set)
+static std::atomic<long long> g_spin_limit_ms{10000};  // a coarse-solve wait longer than this is a fault
+static std::atomic<int> g_force_explicit_rho{0};      // DCGS2: always take the explicit rho pass
+static std::atomic<long long> g_explicit_rho_passes{0};
+
+SpinCfg spin_cfg(const HgPrecond* P) {
+  SpinCfg c;
+  c.fault = P->d_fault;
+  const long long ms = g_spin_limit_ms.load();
+  c.limit_ns = ms > 0 ? (unsigned long long)ms * 1000000ull : 0ull;
+  return c;
+}
+
+// cudaFuncSetAttribute is per device: remember what each (kernel, device)
+// was configured with instead of a process-wide static
+int ensure_func_attrs(const void* func, size_t smem, bool nonportable_cluster) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  HG_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[std::make_pair(func, dev)];
+  if (have >= smem && have != 0) return HG_OK;
+  HG_CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (nonportable_cluster) HG_CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  have = smem > 0 ? smem : 1;
+  return HG_OK;
+}
 
 template <typename T>
 static int upload(T** dptr, const T* host, size_t count, long long* bytes) {
@@ -313,10 +346,54 @@ struct HgOp {
   const double* basis = nullptr;
   long long basis_ldv = 0, basis_ldcol = 0;
   int basis_cols = 0, basis_nv = 0;
+  std::atomic<int> busy{0};  // inside a solve: its workspaces may not be released by another op's memory plan
+};
+
+// ---- memory plan of the Krylov bases
+// Every op keeps its last solve's basis mapped (hg_op_basis); a solve whose
+// worst-case basis does not fit the free device memory first releases the
+// idle bases of the other ops of this process, then splits its batch.
+static std::mutex g_ops_mu;
+static std::set<HgOp*> g_ops;
+
+static size_t op_ws_bytes(const HgOp* op) {
+  size_t b = op->dws.Q.mapped + op->dwsb.Q.mapped + op->bws.V.mapped + op->bws.WV.mapped;
+  if (op->ws.V) b += sizeof(double) * (size_t)op->ws.n * op->ws.cap * (op->ws.weighted ? 2 : 1);
+  return b;
+}
+
+static void op_release_ws(HgOp* op) {
+  op->ws.~Workspace();
+  new (&op->ws) Workspace();
+  op->bws.clear();
+  op->dws.clear();
+  op->dwsb.clear();
+  op->basis = nullptr;
+  op->basis_cols = op->basis_nv = 0;
+}
+
+// release the idle workspaces of every other op; returns the bytes freed
+static size_t release_idle_ops(const HgOp* self) {
+  std::lock_guard<std::mutex> lk(g_ops_mu);
+  size_t freed = 0;
+  for (HgOp* o : g_ops) {
+    if (o == self || o->busy.load()) continue;
+    const size_t b = op_ws_bytes(o);
+    if (b == 0) continue;
+    op_release_ws(o);
+    freed += b;
+  }
+  return freed;
+}
+
+struct BusyScope {
+  HgOp* op;
+  explicit BusyScope(HgOp* o) : op(o) { if (op) op->busy.fetch_add(1); }
+  ~BusyScope() { if (op) op->busy.fetch_sub(1); }
 };
 
 // Orthogonalisation scheme of hg_gmres / hg_gmres_batch (hg_set_orthogonalization).
-static int g_orth = HG_ORTH_DCGS2;
+static thread_local int g_orth = HG_ORTH_DCGS2;  // per host thread (set around one call by the bindings)
 
 // True under CUDA tool injection (Nsight Compute sets NV_NSIGHT_INJECTION_*,
 // the sanitizer NV_SANITIZER_*, others CUDA_INJECTION64_PATH), with
@@ -393,8 +470,58 @@ void stats_collect() {
 }
 }  // namespace
 
+// Under stream capture the graph would run the pre-launched coarse solve and
+// Z^T r as independent nodes: capture the serial order instead.
+static bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs != cudaStreamCaptureStatusNone;
+}
+
+static bool serial_order(cudaStream_t st) { return serial_kernels() || capturing(st); }
+
+// ---- handle faults: a timed-out device wait (fault word 1) or a failed launch
+// in the middle of an apply (2) poisons the handle
+static int precond_fault(const HgPrecond* P) {
+  if (!P || !P->h_fault) return HG_OK;
+  const int f = *reinterpret_cast<volatile const int*>(P->h_fault);
+  if (f == 0) return HG_OK;
+  set_error(f == 1 ? "a device-side wait of the coarse solve timed out (its Z^T r never arrived: failed or starved "
+                     "launch); the preconditioner handle is poisoned, destroy and recreate it"
+                   : "an earlier apply failed part-way through its launches; the preconditioner handle is "
+                     "poisoned, destroy and recreate it");
+  return HG_ERR_CUDA;
+}
+
+static int poison(HgPrecond* P, int status) {
+  if (status == HG_ERR_CUDA && P && P->h_fault && *reinterpret_cast<volatile int*>(P->h_fault) == 0)
+    *reinterpret_cast<volatile int*>(P->h_fault) = 2;
+  return status;
+}
+
+static int op_fault(const HgOp* op) { return op && op->kind == 1 ? precond_fault(op->P) : HG_OK; }
+
+// stream synchronisation of a solve loop + the handle's fault word
+static int sync_check(cudaStream_t st, const HgOp* op, const HgOp* weight) {
+  HG_CUDA_TRY(cudaStreamSynchronize(st));
+  HG_TRY(op_fault(op));
+  return op_fault(weight);
+}
+
+static int precond_apply_core_impl(HgPrecond* P, const double* r, double* out, const double* W, long long ldw,
+                                   int nv, double* partials, int* nb, cudaStream_t st);
+
 static int precond_apply_core(HgPrecond* P, const double* r, double* out, const double* W, long long ldw,
                               int nv, double* partials, int* nb, cudaStream_t st) {
+  HG_TRY(precond_fault(P));
+  return poison(P, precond_apply_core_impl(P, r, out, W, ldw, nv, partials, nb, st));
+}
+
+static int precond_apply_core_impl(HgPrecond* P, const double* r, double* out, const double* W, long long ldw,
+                                   int nv, double* partials, int* nb, cudaStream_t st) {
   if (P->m > 0 && P->d_b0_inv) {
     // dense coarse mode: Z^T r, then (side stream) c -> B0^{-1} c -> Z y beside the local solves
     HG_TRY(launch_zt(P, r, st));
@@ -406,20 +533,22 @@ static int precond_apply_core(HgPrecond* P, const double* r, double* out, const 
   } else if (P->m > 0) {
     HG_CUDA_TRY(cudaEventRecord(P->ev_fork, st));
     HG_CUDA_TRY(cudaStreamWaitEvent(P->aux, P->ev_fork, 0));
-    if (serial_kernels()) {
-      // tools that serialise kernels (profilers, sanitizers, blocking launches):
-      // no kernel may wait on a later one
+    const bool ser = serial_order(st);
+    if (ser) {
+      // tools that serialise kernels (profilers, sanitizers, blocking launches)
+      // and graph capture: no kernel may wait on a later one
       HG_TRY(launch_zt(P, r, P->aux));
-      HG_TRY(launch_coarse_solve(P, P->aux, P->zt_epoch));
+      HG_TRY(launch_coarse_solve(P, P->aux));
     } else {
       // The latency-bound coarse solve is launched FIRST (side stream) so that
       // it holds its SMs before the local solves fill the GPU; it starts its
-      // work when this apply's Z^T r chunks are all counted (device-side wait).
-      HG_TRY(launch_coarse_solve(P, P->aux, P->zt_epoch + (unsigned long long)P->n_zt_items));
+      // work when the Z^T r launch it pairs with (device ticket) has counted
+      // its chunks — a bounded device-side wait (hg_common.cuh SpinGuard).
+      HG_TRY(launch_coarse_solve(P, P->aux));
     }
     HG_TRY(launch_zy(P, P->aux));
     HG_CUDA_TRY(cudaEventRecord(P->ev_join, P->aux));
-    if (!serial_kernels()) HG_TRY(launch_zt(P, r, st));
+    if (!ser) HG_TRY(launch_zt(P, r, st));
   }
   HG_TRY(launch_local_solve(P, r, st));
   if (P->m > 0) HG_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_join, 0));
@@ -429,7 +558,7 @@ static int precond_apply_core(HgPrecond* P, const double* r, double* out, const 
 // coarse solve of the current Z^T r partials on one stream (apply_coarse, profiling)
 static int coarse_solve_serial(HgPrecond* P, cudaStream_t st) {
   if (P->d_b0_inv) return launch_b0_dense(P, st);
-  return launch_coarse_solve(P, st, P->zt_epoch);
+  return launch_coarse_solve(P, st);
 }
 
 // y = op(x); when partials != null also the fused dots of y against W[0..nv)
@@ -463,8 +592,17 @@ static int op_apply_dots(HgOp* op, const double* x, double* y, const double* W, 
   }
 }
 
+static int precond_apply_multi_core_impl(HgPrecond* P, const double* R, long long ldr, double* OUT, long long ldo,
+                                         int nrhs, cudaStream_t st);
+
 static int precond_apply_multi_core(HgPrecond* P, const double* R, long long ldr, double* OUT, long long ldo,
                                     int nrhs, cudaStream_t st) {
+  HG_TRY(precond_fault(P));
+  return poison(P, precond_apply_multi_core_impl(P, R, ldr, OUT, ldo, nrhs, st));
+}
+
+static int precond_apply_multi_core_impl(HgPrecond* P, const double* R, long long ldr, double* OUT, long long ldo,
+                                         int nrhs, cudaStream_t st) {
   if (nrhs < 1 || nrhs > HG_MAX_RHS) {
     set_error("batched apply: nrhs must be in [1, HG_MAX_RHS]");
     return HG_ERR_ARG;
@@ -480,17 +618,18 @@ static int precond_apply_multi_core(HgPrecond* P, const double* R, long long ldr
   } else if (P->m > 0) {
     HG_CUDA_TRY(cudaEventRecord(P->ev_fork, st));
     HG_CUDA_TRY(cudaStreamWaitEvent(P->aux, P->ev_fork, 0));
-    if (serial_kernels()) {
+    const bool ser = serial_order(st);
+    if (ser) {
       HG_TRY(launch_zt_multi(P, R, ldr, nrhs, P->aux));
-      HG_TRY(launch_b0_multi(P, nrhs, P->aux, P->zt_epoch));
+      HG_TRY(launch_b0_multi(P, nrhs, P->aux));
     } else {
       // as the single-RHS apply: the persistent coarse solve first (holds its
-      // SMs), released by the Z^T R chunk counter
-      HG_TRY(launch_b0_multi(P, nrhs, P->aux, P->zt_epoch + (unsigned long long)P->n_zt_items));
+      // SMs), released by the chunk counters of the Z^T R launch it pairs with
+      HG_TRY(launch_b0_multi(P, nrhs, P->aux));
     }
     HG_TRY(launch_zy_multi(P, nrhs, P->aux));
     HG_CUDA_TRY(cudaEventRecord(P->ev_join, P->aux));
-    if (!serial_kernels()) HG_TRY(launch_zt_multi(P, R, ldr, nrhs, st));
+    if (!ser) HG_TRY(launch_zt_multi(P, R, ldr, nrhs, st));
   }
   HG_TRY(launch_local_solve_multi(P, R, ldr, nrhs, st));
   if (P->m > 0) HG_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_join, 0));
@@ -644,14 +783,17 @@ int hg_precond_destroy(HgPrecond* P) {
   release(P->d_cpartm);
   release(P->d_ym);
   release(P->d_b0m_x);
-  release(P->d_b0m_done);
   release(P->d_blkm_done);
+  release(P->d_ticket);
+  if (P->h_fault) cudaFreeHost(P->h_fault);
+  P->h_fault = nullptr;
+  P->d_fault = nullptr;
   release(P->d_tmpm);
   if (P->aux) cudaStreamDestroy(P->aux);
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);
   if (P->ev_join) cudaEventDestroy(P->ev_join);
-  delete P->op_T;
-  delete P->op_W;
+  hg_op_destroy(P->op_T);
+  hg_op_destroy(P->op_W);
   delete P;
   return HG_OK;
 }
@@ -691,6 +833,11 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
   HG_TRY(upload(&P->A.data, D->b_data, (size_t)D->nnz, bytes));
   if (D->dk_data) HG_TRY(upload(&P->A.data2, D->dk_data, (size_t)D->nnz, bytes));
   HG_TRY(upload<double>(&P->d_tmp, nullptr, (size_t)n, bytes));
+  HG_TRY(upload<unsigned long long>(&P->d_ticket, nullptr, 4, bytes));
+  HG_CUDA_TRY(cudaMemset(P->d_ticket, 0, 4 * sizeof(unsigned long long)));
+  HG_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&P->h_fault), sizeof(int), cudaHostAllocMapped));
+  *P->h_fault = 0;
+  HG_CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&P->d_fault), P->h_fault, 0));
 
   // ---- local blocks
   P->n_local = D->n_local;
@@ -823,11 +970,8 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
     HG_CUDA_TRY(cudaMemset(P->d_b0_done, 0, sizeof(unsigned long long)));
     HG_TRY(upload<unsigned long long>(&P->d_zt_done, nullptr, 1, bytes));
     HG_CUDA_TRY(cudaMemset(P->d_zt_done, 0, sizeof(unsigned long long)));
-    P->zt_epoch = 0;
     HG_TRY(upload<unsigned long long>(&P->d_blk_done, nullptr, (size_t)D->n_cblk, bytes));
     HG_CUDA_TRY(cudaMemset(P->d_blk_done, 0, sizeof(unsigned long long) * D->n_cblk));
-    P->zt_calls = 0;
-    P->b0_epoch = 0;
     HG_TRY(upload<double>(&P->d_y, nullptr, (size_t)P->m, bytes));
     if (D->b0_inv) {
       HG_TRY(upload(&P->d_b0_inv, D->b0_inv, (size_t)P->m * P->m, bytes));
@@ -888,6 +1032,7 @@ int hg_precond_apply_T(HgPrecond* P, const double* u, double* out, void* stream)
     return HG_ERR_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  HG_TRY(precond_fault(P));
   HG_TRY(launch_spmv(P->A, P->A.data, u, P->d_tmp, st));
   return precond_apply_core(P, P->d_tmp, out, nullptr, 0, 0, nullptr, nullptr, st);
 }
@@ -898,11 +1043,13 @@ int hg_precond_apply_coarse(HgPrecond* P, const double* r, double* out, void* st
     return HG_ERR_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  HG_TRY(precond_fault(P));
   if (P->m == 0) return launch_fill(P->n, out, 0.0, st);
-  HG_TRY(launch_zt(P, r, st));
-  HG_TRY(coarse_solve_serial(P, st));
-  HG_TRY(launch_zy(P, st));
-  return launch_assemble(P, true, false, out, nullptr, 0, 0, nullptr, nullptr, st);
+  int s = launch_zt(P, r, st);
+  if (s == HG_OK) s = coarse_solve_serial(P, st);
+  if (s == HG_OK) s = launch_zy(P, st);
+  if (s == HG_OK) s = launch_assemble(P, true, false, out, nullptr, 0, 0, nullptr, nullptr, st);
+  return poison(P, s);
 }
 
 int hg_precond_profile(HgPrecond* P, const double* r, double* out, int32_t iters, double* stage_ms,
@@ -912,6 +1059,7 @@ int hg_precond_profile(HgPrecond* P, const double* r, double* out, int32_t iters
     return HG_ERR_ARG;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  HG_TRY(precond_fault(P));
   cudaEvent_t ev[HG_NSTAGES + 1];
   for (auto& e : ev) HG_CUDA_TRY(cudaEventCreate(&e));
   double acc[HG_NSTAGES] = {0, 0, 0, 0, 0};
@@ -941,7 +1089,8 @@ int hg_precond_profile(HgPrecond* P, const double* r, double* out, int32_t iters
   }
   for (auto& e : ev) cudaEventDestroy(e);
   for (int s = 0; s < HG_NSTAGES; ++s) stage_ms[s] = acc[s] / iters;
-  return status;
+  if (status == HG_OK) status = precond_fault(P);
+  return poison(P, status);
 }
 
 int hg_precond_apply_multi(HgPrecond* P, const double* R, int64_t ldr, double* OUT, int64_t ldo, int32_t nrhs,
@@ -959,6 +1108,7 @@ int hg_precond_profile_multi(HgPrecond* P, const double* R, int64_t ldr, double*
     set_error("hg_precond_profile_multi: bad argument");
     return HG_ERR_ARG;
   }
+  HG_TRY(precond_fault(P));
   HG_TRY(multi_prepare(P));
   cudaStream_t st = (cudaStream_t)stream;
   cudaEvent_t ev[HG_NSTAGES + 1];
@@ -969,8 +1119,7 @@ int hg_precond_profile_multi(HgPrecond* P, const double* R, int64_t ldr, double*
     cudaEventRecord(ev[0], st);
     if ((status = launch_zt_multi(P, R, ldr, nrhs, st)) != HG_OK) break;
     cudaEventRecord(ev[1], st);
-    if ((status = (P->d_b0_inv ? launch_b0_dense_multi(P, nrhs, st) : launch_b0_multi(P, nrhs, st, P->zt_epoch))) !=
-        HG_OK)
+    if ((status = (P->d_b0_inv ? launch_b0_dense_multi(P, nrhs, st) : launch_b0_multi(P, nrhs, st))) != HG_OK)
       break;
     cudaEventRecord(ev[2], st);
     if ((status = launch_zy_multi(P, nrhs, st)) != HG_OK) break;
@@ -992,8 +1141,38 @@ int hg_precond_profile_multi(HgPrecond* P, const double* R, int64_t ldr, double*
   }
   for (auto& e : ev) cudaEventDestroy(e);
   for (int s = 0; s < HG_NSTAGES; ++s) stage_ms[s] = acc[s] / iters;
-  return status;
+  if (status == HG_OK) status = precond_fault(P);
+  return poison(P, status);
 }
+
+int hg_precond_status(HgPrecond* P) {
+  if (!P) {
+    set_error("hg_precond_status: null handle");
+    return HG_ERR_ARG;
+  }
+  return precond_fault(P);
+}
+
+int hg_debug_set(HgPrecond* P, int32_t key, int64_t value) {
+  switch (key) {
+    case HG_DEBUG_SPIN_LIMIT_MS:
+      g_spin_limit_ms = value;
+      return HG_OK;
+    case HG_DEBUG_SKIP_ZT:
+      if (!P) break;
+      P->skip_zt = (int)value;
+      return HG_OK;
+    case HG_DEBUG_FORCE_EXPLICIT_RHO:
+      g_force_explicit_rho = value != 0;
+      return HG_OK;
+    default:
+      break;
+  }
+  set_error("hg_debug_set: unknown key or missing handle");
+  return HG_ERR_ARG;
+}
+
+int64_t hg_dcgs2_explicit_passes(void) { return g_explicit_rho_passes.load(); }
 
 int hg_precond_spmv(HgPrecond* P, int which, const double* x, double* y, void* stream) {
   if (!P || !x || !y || (which != 0 && which != 1)) {
@@ -1005,6 +1184,7 @@ int hg_precond_spmv(HgPrecond* P, int which, const double* x, double* y, void* s
     set_error("hg_precond_spmv: D_k not uploaded");
     return HG_ERR_ARG;
   }
+  HG_TRY(precond_fault(P));
   return launch_spmv(P->A, vals, x, y, (cudaStream_t)stream);
 }
 
@@ -1013,6 +1193,7 @@ int hg_local_solve(HgPrecond* P, int s, const double* r_local, double* x_local, 
     set_error("hg_local_solve: bad argument");
     return HG_ERR_ARG;
   }
+  HG_TRY(precond_fault(P));
   return launch_local_solve_single(P, s, r_local, x_local, (cudaStream_t)stream);
 }
 
@@ -1027,6 +1208,10 @@ int hg_op_create_csr(int32_t n, int64_t nnz, const int32_t* indptr, const int32_
   op->n = n;
   op->csr.n = n;
   op->csr.nnz = nnz;
+  {
+    std::lock_guard<std::mutex> lk(g_ops_mu);
+    g_ops.insert(op);
+  }
   int s = HG_OK;
   if ((s = upload(&op->csr.indptr, indptr, (size_t)n + 1, nullptr)) != HG_OK ||
       (s = upload(&op->csr.indices, indices, (size_t)nnz, nullptr)) != HG_OK ||
@@ -1048,12 +1233,30 @@ int hg_op_create_precond(HgPrecond* P, int mode, HgOp** out) {
   op->n = P->n;
   op->P = P;
   op->mode = mode;
+  {
+    std::lock_guard<std::mutex> lk(g_ops_mu);
+    g_ops.insert(op);
+  }
   *out = op;
+  return HG_OK;
+}
+
+int hg_op_release(HgOp* op) {
+  if (!op) {
+    set_error("hg_op_release: null operator");
+    return HG_ERR_ARG;
+  }
+  if (g_shutdown) return HG_OK;
+  op_release_ws(op);
   return HG_OK;
 }
 
 int hg_op_destroy(HgOp* op) {
   if (!op || g_shutdown) return HG_OK;
+  {
+    std::lock_guard<std::mutex> lk(g_ops_mu);
+    g_ops.erase(op);
+  }
   if (op->kind == 0) {
     release(op->csr.indptr);
     release(op->csr.indices);
@@ -1068,6 +1271,7 @@ int hg_op_apply(HgOp* op, const double* x, double* y, void* stream) {
     set_error("hg_op_apply: null argument");
     return HG_ERR_ARG;
   }
+  HG_TRY(op_fault(op));
   return op_apply_dots(op, x, y, nullptr, 0, 0, nullptr, nullptr, (cudaStream_t)stream);
 }
 
@@ -1076,12 +1280,25 @@ int hg_op_apply_multi(HgOp* op, const double* X, int64_t ldx, double* Y, int64_t
     set_error("hg_op_apply_multi: bad argument");
     return HG_ERR_ARG;
   }
+  HG_TRY(op_fault(op));
   return op_apply_multi(op, X, ldx, Y, ldy, nrhs, (cudaStream_t)stream);
 }
 
 // ------------------------------------------------------------------ GMRES
 static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr, double* x, long long ldx, int nrhs,
                        double rtol, int maxit, double* history, int32_t* info, cudaStream_t st);
+
+// The basis kernels (fused dots / updates / x = V y) hold their coefficients
+// in shared memory: at most MAX_NV basis vectors.  Refused up front rather
+// than after ~MAX_NV device iterations.
+static int check_maxit(int maxit) {
+  if (maxit > MAX_NV) {
+    set_error("weighted GMRES: maxit = " + std::to_string(maxit) + " exceeds the " + std::to_string(MAX_NV) +
+              "-vector Krylov basis this library supports (full GMRES keeps every vector)");
+    return HG_ERR_UNSUPPORTED;
+  }
+  return HG_OK;
+}
 
 // Restates wgmres.weighted_gmres (wgmres.py:74-203): classical Gram-Schmidt
 // with the reference's measured, conditional second pass (the measurement
@@ -1101,6 +1318,10 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
   cudaStream_t st = (cudaStream_t)stream;
   const int n = op->n;
   maxit = std::max(0, std::min(maxit, n));
+  HG_TRY(check_maxit(maxit));
+  HG_TRY(op_fault(op));
+  HG_TRY(op_fault(weight));
+  BusyScope busy(op);
   if (g_orth == HG_ORTH_DCGS2) {
     if (!x0) return gmres_dcgs2(op, weight, rhs, n, x, n, 1, rtol, maxit, history, info, st);
     // r0 = rhs - op(x0); x = x0 + GMRES(r0)
@@ -1111,7 +1332,7 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
     if (s == HG_OK) s = gmres_dcgs2(op, weight, r0, n, x, n, 1, rtol, maxit, history, info, st);
     if (s == HG_OK) s = launch_add(n, x, x0, x, st);
     cudaFreeAsync(r0, st);
-    HG_CUDA_TRY(cudaStreamSynchronize(st));
+    HG_TRY(sync_check(st, op, weight));
     return s;
   }
   Workspace& ws = op->ws;
@@ -1137,7 +1358,7 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
     HG_TRY(launch_dots(n, V, nullptr, 0, 0, ws.partials, &nb, st));
   HG_TRY(launch_reduce(ws.partials, nb, 1, ws.dc, st));
   HG_CUDA_TRY(cudaMemcpyAsync(hb, ws.dc, sizeof(double), cudaMemcpyDeviceToHost, st));
-  HG_CUDA_TRY(cudaStreamSynchronize(st));
+  HG_TRY(sync_check(st, op, weight));
   const double beta = std::sqrt(hb[0]);
   if (beta == 0.0) {
     if (x0)
@@ -1147,7 +1368,7 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
     history[0] = 0.0;
     info[0] = 0;
     info[1] = 1;
-    HG_CUDA_TRY(cudaStreamSynchronize(st));
+    HG_TRY(sync_check(st, op, weight));
     return HG_OK;
   }
   HG_TRY(launch_scale2(n, V, WV, &beta, V, weighted ? WV : nullptr, st));
@@ -1186,7 +1407,7 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
     }
     HG_CUDA_TRY(cudaMemcpyAsync(hb, ws.dh + 1, sizeof(double) * nv, cudaMemcpyDeviceToHost, st));
     HG_CUDA_TRY(cudaMemcpyAsync(hb + nv, ws.dc, sizeof(double) * (nv + 1), cudaMemcpyDeviceToHost, st));
-    HG_CUDA_TRY(cudaStreamSynchronize(st));
+    HG_TRY(sync_check(st, op, weight));
     for (int i = 0; i < nv; ++i) col[i] = hb[i];
     double hnorm = std::sqrt(std::max(hb[nv], 0.0));
     double cmax = 0.0;
@@ -1201,7 +1422,7 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
         HG_TRY(launch_dots(n, w, nullptr, 0, 0, ws.partials, &nb, st));
       HG_TRY(launch_reduce(ws.partials, nb, 1, ws.dc, st));
       HG_CUDA_TRY(cudaMemcpyAsync(hb, ws.dc, sizeof(double), cudaMemcpyDeviceToHost, st));
-      HG_CUDA_TRY(cudaStreamSynchronize(st));
+      HG_TRY(sync_check(st, op, weight));
       hnorm = std::sqrt(std::max(hb[0], 0.0));
       ++reorth;
     }
@@ -1261,7 +1482,7 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
   } else if (!x0) {
     HG_TRY(launch_fill(n, x, 0.0, st));
   }
-  HG_CUDA_TRY(cudaStreamSynchronize(st));
+  HG_TRY(sync_check(st, op, weight));
   stats_collect();
   op->basis = V;
   op->basis_ldv = ld;
@@ -1277,16 +1498,9 @@ int hg_gmres(HgOp* op, HgOp* weight, const double* rhs, const double* x0, double
 
 static int ensure_solve_ops(HgPrecond* P) {
   if (!P->op_T) {
-    HgOp* t = new HgOp();
-    t->kind = 1;
-    t->n = P->n;
-    t->P = P;
-    t->mode = 1;
-    HgOp* w = new HgOp();
-    w->kind = 1;
-    w->n = P->n;
-    w->P = P;
-    w->mode = 3;
+    HgOp *t = nullptr, *w = nullptr;
+    HG_TRY(hg_op_create_precond(P, 1, &t));
+    HG_TRY(hg_op_create_precond(P, 3, &w));
     P->op_T = t;
     P->op_W = w;
   }
@@ -1301,14 +1515,15 @@ int hg_solve_host(HgPrecond* P, const double* f_host, double* x_host, double rto
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int n = P->n;
+  HG_TRY(precond_fault(P));
   HG_TRY(ensure_solve_ops(P));
   double *d_f = nullptr, *d_rhs = nullptr, *d_x = nullptr;
   HG_CUDA_TRY(cudaMallocAsync(&d_f, sizeof(double) * n, st));
   HG_CUDA_TRY(cudaMallocAsync(&d_rhs, sizeof(double) * n, st));
   HG_CUDA_TRY(cudaMallocAsync(&d_x, sizeof(double) * n, st));
   HG_CUDA_TRY(cudaMemcpyAsync(d_f, f_host, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-  HG_TRY(precond_apply_core(P, d_f, d_rhs, nullptr, 0, 0, nullptr, nullptr, st));
-  int s = hg_gmres(P->op_T, P->A.data2 ? P->op_W : nullptr, d_rhs, nullptr, d_x, rtol, maxit, history, info,
+  int s = precond_apply_core(P, d_f, d_rhs, nullptr, 0, 0, nullptr, nullptr, st);
+  if (s == HG_OK) s = hg_gmres(P->op_T, P->A.data2 ? P->op_W : nullptr, d_rhs, nullptr, d_x, rtol, maxit, history, info,
                    stream);
   if (s == HG_OK) {
     HG_CUDA_TRY(cudaMemcpyAsync(x_host, d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
@@ -1317,6 +1532,7 @@ int hg_solve_host(HgPrecond* P, const double* f_host, double* x_host, double rto
   cudaFreeAsync(d_rhs, st);
   cudaFreeAsync(d_x, st);
   HG_CUDA_TRY(cudaStreamSynchronize(st));
+  if (s == HG_OK) s = precond_fault(P);
   return s;
 }
 
@@ -1385,8 +1601,51 @@ static bool host_timing() {
 }
 static double g_host_wait = 0.0, g_host_work = 0.0;
 
+static int gmres_dcgs2_run(HgOp* op, HgOp* weight, const double* rhs, long long ldr, double* x, long long ldx,
+                           int nrhs, double rtol, int maxit, double* history, int32_t* info, cudaStream_t st);
+
+// Memory plan: the worst-case basis is nrhs (maxit + 1) n doubles.  If it
+// does not fit the free device memory (plus what this op already holds),
+// the idle bases of the other ops are released first; if it still does not
+// fit, the batch is solved in sub-batches of columns (columns are
+// independent, so only the throughput changes).  The basis is mapped on
+// demand, so a solve that converges early never touches the worst case.
 static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr, double* x, long long ldx, int nrhs,
                        double rtol, int maxit, double* history, int32_t* info, cudaStream_t st) {
+  const size_t per_col = sizeof(double) * (size_t)op->n * (size_t)(maxit + 1);
+  const size_t margin = (size_t)2 << 30;  // workspaces, the operator's scratch, allocator slack
+  auto fits = [&](int cols, size_t& free_b) -> bool {
+    size_t total = 0;
+    free_b = 0;
+    if (cudaMemGetInfo(&free_b, &total) != cudaSuccess) {
+      cudaGetLastError();
+      return true;  // cannot tell: map on demand
+    }
+    const size_t have = op_ws_bytes(op);
+    return per_col * (size_t)cols + margin <= free_b + have;
+  };
+  size_t free_b = 0;
+  if (!fits(nrhs, free_b)) {
+    release_idle_ops(op);
+    if (!fits(nrhs, free_b) && nrhs > 1) {
+      const size_t have = op_ws_bytes(op);
+      const size_t avail = free_b + have > margin ? free_b + have - margin : 0;
+      const int sub = std::max(1, std::min(nrhs - 1, (int)(avail / std::max(per_col, (size_t)1))));
+      for (int c0 = 0; c0 < nrhs; c0 += sub) {
+        const int k = std::min(sub, nrhs - c0);
+        HG_TRY(gmres_dcgs2_run(op, weight, rhs + (long long)c0 * ldr, ldr, x + (long long)c0 * ldx, ldx, k, rtol,
+                               maxit, history + (long long)c0 * (maxit + 1), info + 4 * c0, st));
+      }
+      op->basis = nullptr;  // several sub-bases: not inspectable as one
+      op->basis_cols = op->basis_nv = 0;
+      return HG_OK;
+    }
+  }
+  return gmres_dcgs2_run(op, weight, rhs, ldr, x, ldx, nrhs, rtol, maxit, history, info, st);
+}
+
+static int gmres_dcgs2_run(HgOp* op, HgOp* weight, const double* rhs, long long ldr, double* x, long long ldx,
+                           int nrhs, double rtol, int maxit, double* history, int32_t* info, cudaStream_t st) {
   const int n = op->n;
   const auto t_start = std::chrono::steady_clock::now();
   g_host_wait = g_host_work = 0.0;
@@ -1409,7 +1668,13 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
   const long long W2 = 2LL * (ws.cap + 2), Y2 = ws.cap + 2;
   const long long vstride = (long long)nrhs * n;
   const size_t vbytes = sizeof(double) * (size_t)n;
-  HG_TRY(ws.Q.ensure(vbytes * nrhs));
+  // basis growth; on exhaustion release the other ops' idle bases once and retry
+  auto grow = [&](size_t bytes) -> int {
+    int r = ws.Q.ensure(bytes);
+    if (r == HG_ERR_NOMEM && release_idle_ops(op) > 0) r = ws.Q.ensure(bytes);
+    return r;
+  };
+  HG_TRY(grow(vbytes * nrhs));
   double* Q = ws.Q.ptr();
   auto qv = [&](int i) { return Q + (long long)i * vstride; };
   double* hdots = ws.hbuf;
@@ -1433,7 +1698,7 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
     HG_TRY(launch_reduce_batch(ws.partials, nb, 1, 1, all, ws.nrm2, 1, st));
   }
   HG_CUDA_TRY(cudaMemcpyAsync(hnrm, ws.nrm2, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, st));
-  HG_CUDA_TRY(cudaStreamSynchronize(st));
+  HG_TRY(sync_check(st, op, weight));
 
   struct ColState {
     double beta = 0.0;
@@ -1441,6 +1706,7 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
     std::vector<double> cs, sn, g;
     int hist_len = 1;
     bool converged = false, breakdown = false;
+    int explicit_passes = 0;
   };
   std::vector<ColState> cst(nrhs);
   ColList act{}, zero{};
@@ -1495,6 +1761,16 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
 
   for (int j = 0; act.n > 0; ++j) {
     const int nv = j + 1;
+    if (nrhs > 1 && act.n < nrhs) {
+      // finished columns ride along in the batched operator apply: feed them
+      // zeros (their slot j of the on-demand basis was never written)
+      ColList idle{};
+      bool on[HG_MAX_RHS] = {false};
+      for (int k = 0; k < act.n; ++k) on[act.c[k]] = true;
+      for (int c = 0; c < nrhs; ++c)
+        if (!on[c]) idle.c[idle.n++] = c;
+      HG_TRY(launch_fill_batch(n, qv(j), n, idle, st));
+    }
     {
       Phase ph(st, 0);
       if (nrhs == 1)
@@ -1517,9 +1793,54 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
     HG_CUDA_TRY(cudaMemcpyAsync(hdots, ws.dots, sizeof(double) * 2 * nv * nrhs, cudaMemcpyDeviceToHost, st));
     HG_CUDA_TRY(cudaMemcpyAsync(hnrm, ws.nrm2, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, st));
     const auto th0 = std::chrono::steady_clock::now();
-    HG_CUDA_TRY(cudaStreamSynchronize(st));
+    HG_TRY(sync_check(st, op, weight));
     const auto th1 = std::chrono::steady_clock::now();
 
+    // DCGS2 safety: rho^2 = a_j - s.s loses its digits to cancellation when
+    // q_j is nearly in span(Q) (rho^2 <= 1e-8 a_j leaves < 4 digits in rho).
+    // Those columns take an explicit pass instead: q_j -= Q s on the device,
+    // rho^2 = ||q_j||_W^2 measured directly (one more basis read + W SpMV for
+    // them), and the update then skips the (already applied) correction.
+    double rho2x[HG_MAX_RHS];
+    bool expl[HG_MAX_RHS] = {false};
+    if (j > 0) {
+      ColList ex{};
+      const bool force = g_force_explicit_rho.load() != 0;
+      for (int k = 0; k < act.n; ++k) {
+        const int c = act.c[k];
+        const double* a = hdots + (long long)c * 2 * nv;
+        const std::vector<double>& col = cst[c].Hraw[j - 1];
+        const double beta = std::sqrt(std::max(hnrm[c], 0.0));
+        double cscale = beta;
+        for (int i = 0; i < j; ++i) cscale = std::max(cscale, std::fabs(col[i]));
+        if (beta <= BREAKDOWN_RTOL * std::max(cscale, 1e-300)) continue;  // breakdown: no rho needed
+        double ss = 0.0;
+        for (int i = 0; i < j; ++i) ss += a[i] * a[i];
+        if (force || !(a[j] - ss > 1e-8 * a[j])) {
+          ex.c[ex.n++] = c;
+          expl[c] = true;
+          for (int i = 0; i < j; ++i) hcoef[(long long)c * j + i] = a[i];
+        }
+      }
+      if (ex.n > 0) {
+        HG_CUDA_TRY(cudaMemcpyAsync(ws.coef, hcoef, sizeof(double) * j * nrhs, cudaMemcpyHostToDevice, st));
+        HG_TRY(launch_axpy_batch(n, qv(j), n, Q, vstride, n, j, ws.coef, j, 1, ex, st));  // q_j -= Q s
+        if (weighted) {
+          HG_TRY(wspmv(qv(j), ws.wq, ex, ws.pself, &nbs));
+          HG_TRY(launch_reduce_batch(ws.pself, nbs, 1, 1, ex, ws.dy, 1, st));
+        } else {
+          HG_TRY(launch_dots_batch(n, qv(j), n, nullptr, 0, 0, 0, ex, ws.partials, 1, &nb, st));
+          HG_TRY(launch_reduce_batch(ws.partials, nb, 1, 1, ex, ws.dy, 1, st));
+        }
+        HG_CUDA_TRY(cudaMemcpyAsync(hy, ws.dy, sizeof(double) * nrhs, cudaMemcpyDeviceToHost, st));
+        HG_TRY(sync_check(st, op, weight));
+        for (int k = 0; k < ex.n; ++k) {
+          rho2x[ex.c[k]] = hy[ex.c[k]];
+          ++cst[ex.c[k]].explicit_passes;
+        }
+        g_explicit_rho_passes += ex.n;
+      }
+    }
     ColList keep{}, done{};
     int stopped[HG_MAX_RHS];
     // columns are independent: their host work (Givens, H s) runs in parallel
@@ -1548,8 +1869,9 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
             s[i] = a[i];
             ss += s[i] * s[i];
           }
-          const double rho2 = a[j] - ss;
-          rho = rho2 > 0.0 ? std::sqrt(rho2) : std::sqrt(std::max(a[j], 1e-300));
+          // explicit pass: rho measured on the corrected vector (0 -> breakdown below)
+          const double rho2 = expl[c] ? rho2x[c] : a[j] - ss;
+          rho = std::sqrt(std::max(rho2, 0.0));
           for (int i = 0; i < j; ++i) col[i] += beta * s[i];
           col[j] = beta * rho;
           cscale = 0.0;
@@ -1569,7 +1891,7 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
       cf[0] = 1.0 / rho;
       double sz = 0.0;
       for (int i = 0; i < j; ++i) {
-        cf[1 + i] = s[i];
+        cf[1 + i] = expl[c] ? 0.0 : s[i];  // explicit pass: q_j already corrected on the device
         sz += s[i] * z[i];
       }
       // (H s)_i over the corrected columns 0..j-1, column by column (contiguous
@@ -1594,7 +1916,7 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
       else
         keep.c[keep.n++] = act.c[k];
     }
-    if (keep.n > 0 || done.n > 0) HG_TRY(ws.Q.ensure(vbytes * nrhs * std::min(j + 2, ws.cap)));
+    if (keep.n > 0 || done.n > 0) HG_TRY(grow(vbytes * nrhs * std::min(j + 2, ws.cap)));
     const auto th2 = std::chrono::steady_clock::now();
     if (host_timing()) {
       g_host_wait += std::chrono::duration<double>(th1 - th0).count();
@@ -1622,7 +1944,6 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
                                       st));
       }
     }
-    if (done.n > 0 && j + 1 < ws.cap) HG_TRY(launch_fill_batch(n, qv(j + 1), n, done, st));
     act = keep;
   }
   // x_c = Q_c y_c with y_c = R_c^{-1} g_c (wgmres.py:186-192)
@@ -1648,7 +1969,7 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
     else if (cst[c].beta != 0.0)
       HG_TRY(launch_fill_batch(n, x, ldx, one, st));
   }
-  HG_CUDA_TRY(cudaStreamSynchronize(st));
+  HG_TRY(sync_check(st, op, weight));
   stats_collect();
   op->basis = Q;
   op->basis_ldv = vstride;
@@ -1665,7 +1986,8 @@ static int gmres_dcgs2(HgOp* op, HgOp* weight, const double* rhs, long long ldr,
     info[4 * c] = mlist[c];
     info[4 * c + 1] = cst[c].converged ? 1 : 0;
     info[4 * c + 2] = cst[c].breakdown ? 1 : 0;
-    info[4 * c + 3] = mlist[c] > 0 ? mlist[c] - 1 : 0;  // every column is reorthogonalised once
+    // every column is reorthogonalised once (delayed), plus its explicit rho passes
+    info[4 * c + 3] = (mlist[c] > 0 ? mlist[c] - 1 : 0) + cst[c].explicit_passes;
   }
   return HG_OK;
 }
@@ -1741,6 +2063,10 @@ extern "C" int hg_gmres_batch(HgOp* op, HgOp* weight, const double* rhs, int64_t
   cudaStream_t st = (cudaStream_t)stream;
   const int n = op->n;
   maxit = std::max(0, std::min(maxit, n));
+  HG_TRY(check_maxit(maxit));
+  HG_TRY(op_fault(op));
+  HG_TRY(op_fault(weight));
+  BusyScope busy(op);
   if (g_orth == HG_ORTH_DCGS2) return gmres_dcgs2(op, weight, rhs, ldr, x, ldx, nrhs, rtol, maxit, history, info, st);
   const bool weighted = weight != nullptr;
   BatchWs& ws = op->bws;
@@ -1773,7 +2099,7 @@ extern "C" int hg_gmres_batch(HgOp* op, HgOp* weight, const double* rhs, int64_t
   }
   HG_CUDA_TRY(cudaMemcpy2DAsync(hb, sizeof(double), ws.dc, sizeof(double) * W2, sizeof(double), nrhs,
                                 cudaMemcpyDeviceToHost, st));
-  HG_CUDA_TRY(cudaStreamSynchronize(st));
+  HG_TRY(sync_check(st, op, weight));
 
   struct ColState {
     double beta = 0.0;
@@ -1834,7 +2160,7 @@ extern "C" int hg_gmres_batch(HgOp* op, HgOp* weight, const double* rhs, int64_t
                                   nrhs, cudaMemcpyDeviceToHost, st));
     HG_CUDA_TRY(cudaMemcpy2DAsync(hb2, sizeof(double) * W2, ws.dc, sizeof(double) * W2, sizeof(double) * (nv + 1),
                                   nrhs, cudaMemcpyDeviceToHost, st));
-    HG_CUDA_TRY(cudaStreamSynchronize(st));
+    HG_TRY(sync_check(st, op, weight));
     std::vector<std::vector<double>> cols(nrhs);
     std::vector<double> hnorm(nrhs, 0.0);
     ColList ro{};
@@ -1866,7 +2192,7 @@ extern "C" int hg_gmres_batch(HgOp* op, HgOp* weight, const double* rhs, int64_t
       }
       HG_CUDA_TRY(cudaMemcpy2DAsync(hb2, sizeof(double), ws.dc, sizeof(double) * W2, sizeof(double), nrhs,
                                     cudaMemcpyDeviceToHost, st));
-      HG_CUDA_TRY(cudaStreamSynchronize(st));
+      HG_TRY(sync_check(st, op, weight));
       for (int k = 0; k < ro.n; ++k) hnorm[ro.c[k]] = std::sqrt(std::max(hb2[ro.c[k]], 0.0));
     }
     ColList scl{}, done{}, keep{};
@@ -1944,7 +2270,7 @@ extern "C" int hg_gmres_batch(HgOp* op, HgOp* weight, const double* rhs, int64_t
     else if (cst[c].beta != 0.0)
       HG_TRY(launch_fill_batch(n, x, ldx, one, st));
   }
-  HG_CUDA_TRY(cudaStreamSynchronize(st));
+  HG_TRY(sync_check(st, op, weight));
   stats_collect();
   op->basis = V;
   op->basis_ldv = vstride;
@@ -1969,6 +2295,7 @@ extern "C" int hg_solve_host_batch(HgPrecond* P, const double* F_host, double* X
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int n = P->n;
+  HG_TRY(precond_fault(P));
   HG_TRY(ensure_solve_ops(P));
   const size_t bytes = sizeof(double) * (size_t)n * nrhs;
   double *d_f = nullptr, *d_rhs = nullptr, *d_x = nullptr;
@@ -1985,6 +2312,7 @@ extern "C" int hg_solve_host_batch(HgPrecond* P, const double* F_host, double* X
   cudaFreeAsync(d_rhs, st);
   cudaFreeAsync(d_x, st);
   HG_CUDA_TRY(cudaStreamSynchronize(st));
+  if (s == HG_OK) s = precond_fault(P);
   return s;
 }
 

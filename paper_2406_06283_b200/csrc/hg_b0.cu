@@ -55,32 +55,42 @@ __global__ void __launch_bounds__(THREADS) k_b0_tiles(int m, int K, const int* _
                                                       const long long* __restrict__ tile_ptr,
                                                       const int* __restrict__ tile_col,
                                                       const double* __restrict__ tiles, double* xbuf,
-                                                      unsigned long long* done, unsigned long long base,
+                                                      unsigned long long* done, unsigned long long* ticket,
                                                       double* __restrict__ y,
                                                       const unsigned long long* zt_done,
-                                                      unsigned long long zt_target) {
+                                                      unsigned long long n_zt_items, SpinCfg spin) {
   constexpr int TPR = THREADS / P;  // threads per row
   constexpr int CPT = P / TPR;      // columns per thread
   static_assert(TPR >= 1 && TPR <= 32 && (32 % TPR) == 0 && CPT % 2 == 0, "tile mapping");
   __shared__ __align__(16) double accs[P];
-  __shared__ unsigned long long s_seen;
+  __shared__ unsigned long long s_seen, s_launch;
   const int tid = threadIdx.x, row = tid / TPR, q = tid % TPR, lane = tid & 31;
   const int src = lane - q;  // first lane of this row's group
+  bool dead = false;         // thread 0 only: a bounded wait gave up (the host sees the fault word)
   // s_seen: the counter value this CTA has observed (acquire by thread 0,
   // then a barrier so every thread may read the panels it covers).
   auto observe = [&](unsigned long long need) -> unsigned long long {
     if (tid == 0) {
       unsigned long long v = ld_acquire_u64(done);
-      while (v < need) v = ld_acquire_u64(done);
-      s_seen = v;
+      SpinGuard sg;
+      while (v < need && !dead) {
+        if (spin_abort(sg, spin)) dead = true;
+        v = ld_acquire_u64(done);
+      }
+      s_seen = dead ? ~0ull : v;
     }
     __syncthreads();
     return s_seen;
   };
-  if (tid == 0)  // c = Z^T r of this apply complete (the solve may be launched before it)
-    while (ld_acquire_u64(zt_done) < zt_target) {
-    }
+  if (tid == 0) {  // c = Z^T r of this apply complete (the solve may be launched before it)
+    s_launch = take_launch_index(ticket, gridDim.x);
+    const unsigned long long zt_target = (s_launch + 1) * n_zt_items;
+    SpinGuard sg;
+    while (ld_acquire_u64(zt_done) < zt_target && !dead)
+      if (spin_abort(sg, spin)) dead = true;
+  }
   __syncthreads();
+  const unsigned long long base = s_launch * 2ull * (unsigned long long)K;  // done counter at this launch's start
   for (int g = blockIdx.x; g < 2 * K; g += gridDim.x) {
     const int ph = g / K, t = g % K;
     const bool stamp = g_b0_stamp_on && tid == 0 && g < B0_MAX_STAMPED;
@@ -166,8 +176,9 @@ __global__ void __launch_bounds__(THREADS) k_b0_tiles(int m, int K, const int* _
     if (tid == 0) {
       // the release store is cumulative over the CTA's x stores ordered before
       // it by the barrier; publish in panel order (a panel may finish first)
-      while (ld_acquire_u64(done) < base + g) {
-      }
+      SpinGuard sg;
+      while (ld_acquire_u64(done) < base + g && !dead)
+        if (spin_abort(sg, spin)) dead = true;
       st_release_u64(done, base + g + 1);
       if (stamp) g_b0_stamps[3 * g + 2] = gtimer();
     }
@@ -182,28 +193,28 @@ int preload_b0() {
   return preload_b0_cluster();
 }
 
-int launch_coarse_solve(HgPrecond* P, cudaStream_t st, unsigned long long zt_target) {
+int launch_coarse_solve(HgPrecond* P, cudaStream_t st) {
   if (P->m == 0) return HG_OK;
-  if (P->b0_mode == 1) return launch_coarse_solve_cluster(P, st, zt_target);
+  if (P->b0_mode == 1) return launch_coarse_solve_cluster(P, st);
   const int K = P->b0_K;
   const int G = K < P->b0_ctas ? K : P->b0_ctas;
-  const unsigned long long base = P->b0_epoch;
-  P->b0_epoch += 2ull * K;
+  const unsigned long long nzt = (unsigned long long)P->n_zt_items;
+  const SpinCfg spin = spin_cfg(P);
   switch (P->b0_P) {
     case 64:
       k_b0_tiles<64, 256><<<G, 256, 0, st>>>(P->m, K, P->d_b0_perm, P->d_col_blk, P->d_cblk, P->d_cpart,
                                               P->d_b0_dinv, P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles,
-                                              P->d_b0_x, P->d_b0_done, base, P->d_y, P->d_zt_done, zt_target);
+                                              P->d_b0_x, P->d_b0_done, P->d_ticket, P->d_y, P->d_zt_done, nzt, spin);
       break;
     case 128:
       k_b0_tiles<128, 512><<<G, 512, 0, st>>>(P->m, K, P->d_b0_perm, P->d_col_blk, P->d_cblk, P->d_cpart,
                                                P->d_b0_dinv, P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles,
-                                               P->d_b0_x, P->d_b0_done, base, P->d_y, P->d_zt_done, zt_target);
+                                               P->d_b0_x, P->d_b0_done, P->d_ticket, P->d_y, P->d_zt_done, nzt, spin);
       break;
     case 32:
       k_b0_tiles<32, 128><<<G, 128, 0, st>>>(P->m, K, P->d_b0_perm, P->d_col_blk, P->d_cblk, P->d_cpart,
                                               P->d_b0_dinv, P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles,
-                                              P->d_b0_x, P->d_b0_done, base, P->d_y, P->d_zt_done, zt_target);
+                                              P->d_b0_x, P->d_b0_done, P->d_ticket, P->d_y, P->d_zt_done, nzt, spin);
       break;
     default:
       set_error("coarse solve: unsupported panel size");

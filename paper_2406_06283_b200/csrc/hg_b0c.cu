@@ -103,10 +103,12 @@ __device__ __forceinline__ int swz(int row, int c) { return c ^ ((row & 1) << 2)
 // Entries 2(q+4k), 2(q+4k)+1 (k = 0..7) of panel g from the tagged ring;
 // spins until all 16 tags read g.  The 4 threads of a row group together
 // cover all CP entries.
-__device__ __forceinline__ void poll_panel(const double* xring, int g, int NR, int q, double (&xv)[16]) {
+__device__ __forceinline__ void poll_panel(const double* xring, int g, int NR, int q, double (&xv)[16],
+                                           const SpinCfg& spin, bool& dead) {
   const double* slot = xring + (size_t)(g % NR) * CP * 2;
   const double tag = (double)g;
   bool ok;
+  SpinGuard sg;
   do {
     ok = true;
 #pragma unroll
@@ -117,6 +119,10 @@ __device__ __forceinline__ void poll_panel(const double* xring, int g, int NR, i
       xv[2 * k] = p0.x;
       xv[2 * k + 1] = p1.x;
       ok = ok && (p0.y == tag) && (p1.y == tag);
+    }
+    if (!ok && (dead || spin_abort(sg, spin))) {  // bounded: a faulted handle finishes on garbage
+      dead = true;
+      ok = true;
     }
   } while (!__all_sync(FULL, ok));
 }
@@ -151,7 +157,9 @@ struct B0ClusterArgs {
   double* xbuf;             // [2][K*P] global copy of the solved panels
   double* y;
   const unsigned long long* blk_done;  // per coarse block Z^T r chunk counters
-  unsigned long long zt_calls;         // block b of c is complete at zt_calls * nchunk_b
+  unsigned long long* ticket;          // launch L (take_launch_index) reads Z^T r launch L:
+                                       // block b of c is complete at (L + 1) nchunk_b
+  SpinCfg spin;
 };
 
 __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
@@ -163,11 +171,13 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
   uint64_t* tempty = tfull + TNS;
   uint64_t* ldone = tempty + TNS;                       // the whole L solve is in global memory
 
+  __shared__ unsigned long long s_launch;
   const int tid = threadIdx.x;
   const uint32_t rank = cluster_rank();
   const int CS = a.CS, K = a.K, NR = a.NR;
   for (int i = tid; i < NR * CP; i += CTHREADS) xring[2 * i + 1] = -1.0;  // no panel yet
   if (tid == 0) {
+    s_launch = take_launch_index(a.ticket, CS);
     for (int s = 0; s < TNS; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], CONS / 32);
@@ -198,6 +208,8 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
     const int row = tid >> 2, q = tid & 3, lane = tid & 31;
     int c = 0;  // tile-stream position
     bool l_done = false;
+    bool dead = false;  // a bounded wait gave up: finish on garbage, the host reports the fault
+    const unsigned long long zt_launches = s_launch + 1;
     for (int g = rank; g < 2 * K; g += CS) {
       const int ph = g / K, t = g % K;
       const bool stamp = g_b0c_stamp_on && tid == 0 && g < 8192;
@@ -213,11 +225,10 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
             const int col = a.perm[i];
             const int b = a.col_blk[col];
             const CblkDesc d = a.descs[b];
-            const unsigned long long need = a.zt_calls * (unsigned long long)d.nchunk;
-            unsigned long long got;
-            do {
-              asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(got) : "l"(a.blk_done + b) : "memory");
-            } while (got < need);
+            const unsigned long long need = zt_launches * (unsigned long long)d.nchunk;
+            SpinGuard sg;
+            while (!dead && ld_acquire_gpu_u64(a.blk_done + b) < need)
+              if (spin_abort(sg, a.spin)) dead = true;
             const int l = col - d.col0;
             for (int ch = 0; ch < d.nchunk; ++ch) v += a.cpart[d.part_off + (long long)ch * d.m + l];
           }
@@ -251,7 +262,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
       for (long long e = e0; e < e1; ++e, ++c) {
         const int gj = ph * K + a.tile_col[e];
         if (stamp && gj == g - 1) g_b0c_stamps[4 * g + 1] = gtimer_b0c();
-        poll_panel(xring, gj, NR, q, xv);
+        poll_panel(xring, gj, NR, q, xv, a.spin, dead);
         if (gj == g - 1) {
           saw_prev = true;
           if (stamp) g_b0c_stamps[4 * g + 2] = gtimer_b0c();
@@ -263,7 +274,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
         if (lane == 0) mbar_arrive(&tempty[stage]);
       }
       // in-order publication: this row group has seen all of x_{g-1}
-      if (!saw_prev) poll_panel(xring, g - 1, NR, q, xv);
+      if (!saw_prev) poll_panel(xring, g - 1, NR, q, xv, a.spin, dead);
       const uint32_t slot_addr = smem_u32(xring + ((size_t)(g % NR) * CP + row) * 2);
       const uint32_t nxt = (rank + 1) % CS;
       const double tag = (double)g;
@@ -291,7 +302,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
     for (int s2 = 0; s2 < NR && s2 < 2 * K; ++s2) {
       const int glast = s2 + ((2 * K - 1 - s2) / NR) * NR;
       double tmp[16];
-      poll_panel(xring, glast, NR, q, tmp);
+      poll_panel(xring, glast, NR, q, tmp, a.spin, dead);
     }
   }
   __syncthreads();
@@ -309,19 +320,14 @@ int preload_b0_cluster() {
   return HG_OK;
 }
 
-int launch_coarse_solve_cluster(HgPrecond* P, cudaStream_t st, unsigned long long zt_target) {
+int launch_coarse_solve_cluster(HgPrecond* P, cudaStream_t st) {
   const int K = P->b0_K;
   const int CS = P->b0_cs;
   B0ClusterArgs a{P->m, K, P->b0_nr, CS, P->d_b0_perm, P->d_col_blk, P->d_cblk, P->d_cpart, P->d_b0_dinv,
                   P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles, P->d_b0_x, P->d_y,
-                  P->d_blk_done, P->zt_calls + (zt_target > P->zt_epoch ? 1ull : 0ull)};
+                  P->d_blk_done, P->d_ticket, spin_cfg(P)};
   const size_t smem = b0_cluster_smem(P->b0_nr);
-  static size_t configured = 0;
-  if (configured < smem) {
-    HG_CUDA_TRY(cudaFuncSetAttribute(k_b0_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    HG_CUDA_TRY(cudaFuncSetAttribute(k_b0_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = smem;
-  }
+  HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k_b0_cluster), smem, true));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CS);
   cfg.blockDim = dim3(CTHREADS);

@@ -95,4 +95,62 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
 
+// ---- bounded spin waits
+// Every cross-CTA / cross-kernel wait in this library polls through a
+// SpinGuard: each 256 failed polls it reads the handle's fault word (host
+// mapped, so the host sees it without an API call) and %globaltimer; past
+// `limit_ns` it raises the fault and the wait gives up.  A kernel whose wait
+// gave up finishes its loops on garbage (it never leaves a barrier its peers
+// wait on), and every later wait on a faulted handle gives up at once; the
+// host turns the fault into HG_ERR_CUDA and poisons the handle.
+struct SpinCfg {
+  volatile int* fault;          // device alias of the handle's pinned fault word
+  unsigned long long limit_ns;  // 0 = no limit
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct SpinGuard {
+  unsigned long long t0 = 0;
+  unsigned n = 0;
+};
+
+// true = stop waiting (timeout raised here, or the handle already faulted)
+__device__ __forceinline__ bool spin_abort(SpinGuard& g, const SpinCfg& cfg) {
+  if ((++g.n & 255u) != 0u) return false;
+  if (cfg.fault && *cfg.fault) return true;
+  const unsigned long long t = global_ns();
+  if (g.t0 == 0) {
+    g.t0 = t;
+    return false;
+  }
+  if (cfg.limit_ns && t - g.t0 > cfg.limit_ns) {
+    if (cfg.fault) {
+      *cfg.fault = 1;
+      __threadfence_system();
+    }
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Launch index of a coarse solve from its device ticket counter: every CTA
+// of a launch takes one ticket, launches on a handle are stream ordered, so
+// CTAs of launch L hold tickets [L * ctas, (L + 1) * ctas).  The t-th coarse
+// solve pairs with the t-th Z^T r launch (whose chunks bump the per-block
+// counters), also under CUDA-graph replay — no host-side epoch is baked in.
+__device__ __forceinline__ unsigned long long take_launch_index(unsigned long long* ticket, unsigned ctas) {
+  return atomicAdd(ticket, 1ull) / ctas;
+}
+
 }  // namespace hg

@@ -67,20 +67,26 @@ struct HgPrecond {
   int b0_P = 0, b0_K = 0, b0_ctas = 32;   // panel size, panels per phase, persistent CTAs
   int b0_mode = 0;                        // 0: L2-counter kernel (hg_b0.cu), 1: cluster kernel (hg_b0c.cu)
   int b0_cs = 0, b0_nr = 0;               // cluster size, x ring slots (mode 1)
-  unsigned long long b0_epoch = 0;        // value of the completion counter at the next launch
   double* d_b0_dinv = nullptr;            // [2][K][P][P]
   long long* d_b0_tile_ptr = nullptr;     // [2K+1]
   int* d_b0_tile_col = nullptr;
   double* d_b0_tiles = nullptr;           // [ntile][P][P]
   double* d_b0_x = nullptr;               // [2][K*P] phase solutions
-  unsigned long long* d_b0_done = nullptr;  // monotone panel completion counter
-  unsigned long long* d_zt_done = nullptr;  // monotone count of finished Z^T r chunks
-  unsigned long long zt_epoch = 0;          // its value after the last launched Z^T r
-  unsigned long long b0_zt_target = 0;      // chunks the next coarse solve waits for
+  unsigned long long* d_b0_done = nullptr;  // monotone panel completion counter (mode 0: 2K per launch)
+  unsigned long long* d_zt_done = nullptr;  // monotone count of finished single-RHS Z^T r chunks
   unsigned long long* d_blk_done = nullptr; // per coarse block: monotone count of its finished single-RHS Z^T r chunks
-  unsigned long long zt_calls = 0;          // single-RHS Z^T r launches so far (block b is complete at zt_calls * nchunk_b)
   unsigned long long* d_blkm_done = nullptr;  // the same for the batched Z^T R
-  unsigned long long ztm_calls = 0;
+  // device tickets of the coarse solves ([0] single, [1] batched): the L-th
+  // coarse launch waits for the (L+1)-th Z^T r launch (take_launch_index);
+  // nothing about the pairing lives on the host, so CUDA-graph replays and
+  // eager calls interleave safely
+  unsigned long long* d_ticket = nullptr;
+  // bounded waits: pinned, host-mapped fault word (hg_common.cuh SpinGuard);
+  // nonzero = a wait timed out or a launch failed mid-apply: the handle is
+  // poisoned and every later call fails with HG_ERR_CUDA
+  int* h_fault = nullptr;
+  int* d_fault = nullptr;
+  int skip_zt = 0;                // fault injection (hg_debug_set): Z^T r launches to drop
   double* d_y = nullptr;          // coarse solution (m)
   double* d_b0_inv = nullptr;     // dense B0^{-1} (m x m row-major) or null
   double* d_c = nullptr;          // reduced Z^T r (m), dense mode
@@ -100,8 +106,6 @@ struct HgPrecond {
   double* d_cpartm = nullptr;     // [part_len][HG_MAX_RHS] Z^T R partials
   double* d_ym = nullptr;         // [m][HG_MAX_RHS] coarse solution
   double* d_b0m_x = nullptr;      // [2][K*64][HG_MAX_RHS] phase solutions
-  unsigned long long* d_b0m_done = nullptr;  // monotone panel counter of the batched coarse solve
-  unsigned long long b0m_epoch = 0;
   double* d_tmpm = nullptr;       // [c][n] scratch (B U for the batched apply_T)
   cudaStream_t aux = nullptr;     // coarse chain runs here, forked/joined per apply
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -167,8 +171,12 @@ int preload_local_blocked();
 int launch_local_solve_single(HgPrecond* P, int s, const double* r_local, double* x_local, cudaStream_t st);
 int launch_zt(HgPrecond* P, const double* r, cudaStream_t st);
 // zt_target: value of the Z^T r chunk counter the solve waits for before reading c
-int launch_coarse_solve(HgPrecond* P, cudaStream_t st, unsigned long long zt_target);
-int launch_coarse_solve_cluster(HgPrecond* P, cudaStream_t st, unsigned long long zt_target);
+// the solve waits (bounded, device side) for the Z^T r launch it pairs with
+int launch_coarse_solve(HgPrecond* P, cudaStream_t st);
+int launch_coarse_solve_cluster(HgPrecond* P, cudaStream_t st);
+SpinCfg spin_cfg(const HgPrecond* P);
+// per (kernel, device) dynamic shared memory / cluster attributes (thread safe)
+int ensure_func_attrs(const void* func, size_t smem, bool nonportable_cluster);
 size_t b0_cluster_smem(int NR);
 // force-load kernels at handle creation (see preload_local in hg_local.cu)
 int preload_local(HgPrecond* P);
@@ -201,7 +209,7 @@ int launch_spmm_cols(const DevCsr& A, const double* vals, const double* X, long 
 int launch_spmm_self(const DevCsr& A, const double* vals, const double* X, long long ldx, double* Y,
                      long long ldy, int nrhs, double* partials, int width, int* nblocks_out, cudaStream_t st);
 int launch_zt_multi(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st);
-int launch_b0_multi(HgPrecond* P, int nrhs, cudaStream_t st, unsigned long long zt_target);
+int launch_b0_multi(HgPrecond* P, int nrhs, cudaStream_t st);
 // dense coarse mode (hg_b0d.cu): c = reduce(Z^T r partials), y = B0^{-1} c
 int launch_b0_dense(HgPrecond* P, cudaStream_t st);
 int launch_b0_dense_multi(HgPrecond* P, int nrhs, cudaStream_t st);

@@ -304,18 +304,14 @@ int launch_local_blocked(HgPrecond* P, const double* R, long long ldr, int nrhs,
   int wrows = 0;
   const size_t smem = local_blocked_smem(P, &wrows);
   const int stage_stride = BCH * (P->max_fstride > P->max_bstride ? P->max_fstride : P->max_bstride);
-  static size_t configured = 0;
-  static bool timing_set = false;
+  static bool timing_set = false;  // timing experiments only
   if (!timing_set) {
     const char* tm = getenv("HG_BLK_TIMING");
     int on = (tm && tm[0] == '1') ? 1 : 0;
     HG_CUDA_TRY(cudaMemcpyToSymbol(blk_timing_on, &on, sizeof(int)));
     timing_set = true;
   }
-  if (configured < smem) {
-    HG_CUDA_TRY(cudaFuncSetAttribute(k_local_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
+  HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k_local_blocked), smem, false));
   k_local_blocked<<<P->n_local, BTHREADS, smem, st>>>(P->d_local, P->d_local_idx, P->d_fwd, P->d_bwd, R, ldr,
                                                        P->d_xsm, P->xs_len, nrhs, stage_stride, wrows);
   HG_LAUNCH_CHECK();

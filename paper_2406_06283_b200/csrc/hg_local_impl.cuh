@@ -388,11 +388,7 @@ static int launch_local_grid_t(HgPrecond* P, const LocalDesc* descs, int nblocks
   }
   const int stage_stride = LS_CH * (P->max_fstride > P->max_bstride ? P->max_fstride : P->max_bstride);
   const size_t smem = (size_t)LS_NS * stage_stride * sizeof(double);
-  static size_t configured[7][11] = {};
-  if (configured[P->rf][P->rb] < smem) {
-    HG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured[P->rf][P->rb] = smem;
-  }
+  HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k), smem, false));
   static const int dbg = getenv("HG_LOCAL_DEBUG") ? atoi(getenv("HG_LOCAL_DEBUG")) : 0;  // timing experiments only
   const int nwarps = NW == 1 ? 1 : (nrhs + LS_KM - 1) / LS_KM;  // consumer warps
   k<<<nblocks, 32 * (nwarps + 1), smem, st>>>(descs, P->d_local_idx, P->d_fwd, P->d_bwd, r, xs ? xs : P->d_xs,

@@ -124,7 +124,7 @@ int launch_spmm_self(const DevCsr& A, const double* vals, const double* X, long 
 __global__ void __launch_bounds__(256) k_zt_multi(const int2* __restrict__ items, const CblkDesc* __restrict__ descs,
                                                   const int* __restrict__ idx, const double* __restrict__ Z,
                                                   const double* __restrict__ R, long long ldr, int nrhs,
-                                                  double* __restrict__ cpartm, unsigned long long* __restrict__ done,
+                                                  double* __restrict__ cpartm,
                                                   unsigned long long* __restrict__ blk_done) {
   __shared__ __align__(16) double s_r[ZROWS * SR];
   const int2 it = items[blockIdx.x];
@@ -159,18 +159,19 @@ __global__ void __launch_bounds__(256) k_zt_multi(const int2* __restrict__ items
   __syncthreads();
   if (threadIdx.x == 0) {  // chunk complete: the batched coarse solve may be waiting for it
     __threadfence();
-    atomicAdd(done, 1ull);
     atomicAdd(blk_done + it.x, 1ull);
   }
 }
 
 int launch_zt_multi(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st) {
   if (P->m == 0 || P->n_zt_items == 0) return HG_OK;
+  if (P->skip_zt > 0) {  // fault injection (hg_debug_set)
+    --P->skip_zt;
+    return HG_OK;
+  }
   k_zt_multi<<<P->n_zt_items, 256, 0, st>>>(P->d_zt_items, P->d_cblk, P->d_cblk_idx, P->d_z, R, ldr, nrhs,
-                                             P->d_cpartm, P->d_zt_done, P->d_blkm_done);
+                                             P->d_cpartm, P->d_blkm_done);
   HG_LAUNCH_CHECK();
-  P->zt_epoch += (unsigned long long)P->n_zt_items;
-  P->ztm_calls += 1;
   return HG_OK;
 }
 
@@ -283,9 +284,11 @@ struct B0MultiArgs {
   const double* tiles;      // [ntile][64][64]
   double* xbuf;             // [2K][64][MR] (value, tag) pairs: 2 doubles each
   double* y;                // [m][MR]
-  double tag0;              // tag of panel g in this launch: tag0 + g (unique across launches)
   const unsigned long long* blk_done;  // per coarse block Z^T R chunk counters
-  unsigned long long zt_calls;         // block b complete at zt_calls * nchunk_b
+  unsigned long long* ticket;          // launch index (take_launch_index): launch L reads Z^T R launch L
+                                       // (block b complete at (L + 1) nchunk_b) and tags panel g with
+                                       // 1 + 2K L + g (unique across launches, exact in a double)
+  SpinCfg spin;
 };
 
 // 16-byte (value, tag) pair access: written and read as one vector access,
@@ -303,11 +306,12 @@ __device__ __forceinline__ double2 ld_pair(const double* p) {
 // pair carries the panel's tag: the data is its own completion flag, so a hop
 // costs one L2 round trip (no counter, no fence, no ordered publication).
 __device__ __forceinline__ void wait_panel(const double* __restrict__ xbuf, int gp, double tag, double* s_x,
-                                           bool reversed, int K) {
+                                           bool reversed, int K, const SpinCfg& spin, bool& dead) {
   // thread t covers pairs t, t + 256, t + 512, t + 768 of the panel (rows r = e / MR)
   const double* base = xbuf + (size_t)gp * BP * MR * 2;
   double v[4];
   bool ok;
+  SpinGuard sg;
   do {
     ok = true;
 #pragma unroll
@@ -316,6 +320,10 @@ __device__ __forceinline__ void wait_panel(const double* __restrict__ xbuf, int 
       const double2 p = ld_pair(base + 2 * e);
       v[q] = p.x;
       ok = ok && (p.y == tag);
+    }
+    if (!ok && (dead || spin_abort(sg, spin))) {  // bounded: give up on a faulted handle
+      dead = true;
+      ok = true;
     }
   } while (!ok);
 #pragma unroll
@@ -336,9 +344,15 @@ __device__ __forceinline__ void wait_panel(const double* __restrict__ xbuf, int 
 // over as tagged pairs in global memory (wait_panel).
 __global__ void __launch_bounds__(256, 1) k_b0_multi(B0MultiArgs a) {
   __shared__ __align__(16) double s_x[BP * SR];
+  __shared__ unsigned long long s_launch;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = lane & 3, g8 = lane >> 2;
   const int row = warp * 8 + g8;
   const int K = a.K;
+  if (tid == 0) s_launch = take_launch_index(a.ticket, gridDim.x);
+  __syncthreads();
+  const unsigned long long L = s_launch;
+  const double tag0 = 1.0 + 2.0 * (double)K * (double)L;
+  bool dead = false;
   for (int g = blockIdx.x; g < 2 * K; g += gridDim.x) {
     const int ph = g / K, t = g % K;
     const double* dinv_g = a.dinv + (size_t)g * BTILE;
@@ -355,16 +369,17 @@ __global__ void __launch_bounds__(256, 1) k_b0_multi(B0MultiArgs a) {
           const int col = a.perm[i];
           const int b = a.col_blk[col];
           const CblkDesc d = a.descs[b];
-          const unsigned long long need = a.zt_calls * (unsigned long long)d.nchunk;
-          while (ld_acq(a.blk_done + b) < need) {
-          }
+          const unsigned long long need = (L + 1) * (unsigned long long)d.nchunk;
+          SpinGuard sg;
+          while (!dead && ld_acq(a.blk_done + b) < need)
+            if (spin_abort(sg, a.spin)) dead = true;
           const int l = col - d.col0;
           for (int ch = 0; ch < d.nchunk; ++ch) v += a.cpartm[(d.part_off + (long long)ch * d.m + l) * MR + c];
         }
         s_x[r * SR + c] = v;
       }
     } else {  // the reversed L solution of panel K-1-t
-      wait_panel(a.xbuf, K - 1 - t, a.tag0 + (K - 1 - t), s_x, true, K);
+      wait_panel(a.xbuf, K - 1 - t, tag0 + (K - 1 - t), s_x, true, K, a.spin, dead);
     }
     __syncthreads();
     double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
@@ -381,7 +396,7 @@ __global__ void __launch_bounds__(256, 1) k_b0_multi(B0MultiArgs a) {
       const int gj = ph * K + a.tile_col[e];
       load_afrag(av, a.tiles + (size_t)e * BTILE, row, q, a.swz, -1.0);  // in flight across the wait
       __syncthreads();  // s_x free
-      wait_panel(a.xbuf, gj, a.tag0 + gj, s_x, false, K);
+      wait_panel(a.xbuf, gj, tag0 + gj, s_x, false, K, a.spin, dead);
       __syncthreads();
       mma_tile(acc, av, s_x, q, g8);
     }
@@ -395,7 +410,7 @@ __global__ void __launch_bounds__(256, 1) k_b0_multi(B0MultiArgs a) {
       mma_tile(acc, av, s_x, q, g8);
     }
     // publish: every value with the panel's tag (no fence: each pair is its own flag)
-    const double tag = a.tag0 + g;
+    const double tag = tag0 + g;
     double* xo = a.xbuf + ((size_t)g * BP + row) * MR * 2;
     st_pair(xo + 2 * (2 * q), acc[0][0], tag);
     st_pair(xo + 2 * (2 * q + 1), acc[0][1], tag);
@@ -412,7 +427,7 @@ __global__ void __launch_bounds__(256, 1) k_b0_multi(B0MultiArgs a) {
   }
 }
 
-int launch_b0_multi(HgPrecond* P, int nrhs, cudaStream_t st, unsigned long long zt_target) {
+int launch_b0_multi(HgPrecond* P, int nrhs, cudaStream_t st) {
   if (P->m == 0) return HG_OK;
   if (P->b0_P != BP) {
     set_error("batched coarse solve: needs 64-row panels (HG_B0_PANEL=64)");
@@ -424,9 +439,7 @@ int launch_b0_multi(HgPrecond* P, int nrhs, cudaStream_t st, unsigned long long 
   // tags stay below 2^53 (exact in a double) for ~10^12 launches
   B0MultiArgs a{P->m, K, nrhs, P->b0_mode == 1 ? 1 : 0, P->b0_mode == 1 ? 1 : 0, P->d_b0_perm, P->d_col_blk,
                 P->d_cblk, P->d_cpartm, P->d_b0_dinv, P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles,
-                P->d_b0m_x, P->d_ym, (double)(P->b0m_epoch + 1), P->d_blkm_done,
-                P->ztm_calls + (zt_target > P->zt_epoch ? 1ull : 0ull)};
-  P->b0m_epoch += 2ull * K;
+                P->d_b0m_x, P->d_ym, P->d_blkm_done, P->d_ticket + 1, spin_cfg(P)};
   k_b0_multi<<<G, 256, 0, st>>>(a);
   HG_LAUNCH_CHECK();
   return HG_OK;
@@ -634,10 +647,6 @@ int multi_prepare(HgPrecond* P) {
     }
     HG_CUDA_TRY(cudaMalloc(&P->d_blkm_done, sizeof(unsigned long long) * P->n_cblk));
     HG_CUDA_TRY(cudaMemset(P->d_blkm_done, 0, sizeof(unsigned long long) * P->n_cblk));
-    P->ztm_calls = 0;
-    HG_CUDA_TRY(cudaMalloc(&P->d_b0m_done, sizeof(unsigned long long)));
-    HG_CUDA_TRY(cudaMemset(P->d_b0m_done, 0, sizeof(unsigned long long)));
-    P->b0m_epoch = 0;
   }
   HG_CUDA_TRY(cudaDeviceSynchronize());
   P->multi_ready = true;

@@ -187,6 +187,10 @@ _G = {}
 def _gevp_worker(i):
     forms, dec, method, n_wanted = _G["args"]
     if _G.get("pool"):
+        # one BLAS thread per pool worker: the eigenvectors do not depend on the
+        # worker count, so committed large-config fixtures reproduce on another
+        # host (the serial path keeps the default threads, as the reference's
+        # own golden run did)
         from threadpoolctl import threadpool_limits
 
         with threadpool_limits(1):

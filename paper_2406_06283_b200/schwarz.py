@@ -398,12 +398,23 @@ class TwoLevelPreconditioner:
     def device_bytes(self):
         return int(_lib.load().hg_precond_device_bytes(self._handle))
 
+    def check(self):
+        """Raise DeviceError if a device-side wait of this handle timed out or
+        an apply failed part-way (hg_precond_status; the handle is then
+        poisoned).  Numpy-returning calls check after their copy back; for
+        device-tensor results call this after synchronising."""
+        _lib.check(_lib.load().hg_precond_status(self._handle), "hg_precond_status")
+
     def _run(self, fn, v):
         torch = _torch()
         t, was_np = _as_device(v, self.n)
         out = torch.empty_like(t)
         _lib.check(getattr(_lib.load(), fn)(self._handle, _vp(t), _vp(out), _stream()), fn)
-        return out.cpu().numpy() if was_np else out
+        if was_np:
+            res = out.cpu().numpy()
+            self.check()
+            return res
+        return out
 
     def apply(self, r):
         """M^{-1} r (schwarz.py:51-61); returns a new array."""
@@ -420,7 +431,10 @@ class TwoLevelPreconditioner:
             _lib.load().hg_precond_apply_multi(self._handle, _vp(t), self.n, _vp(out), self.n, t.shape[0], _stream()),
             "hg_precond_apply_multi",
         )
-        return _from_device_batch(out, was_np)
+        res = _from_device_batch(out, was_np)
+        if was_np:
+            self.check()
+        return res
 
     def profile_multi(self, R, iters=5):
         """Mean device ms per stage of the batched apply (stages serialised)."""
@@ -549,12 +563,20 @@ class DeviceOperator:
         t, was_np = _as_device(v, self.n)
         out = torch.empty_like(t)
         _lib.check(_lib.load().hg_op_apply(self._handle, _vp(t), _vp(out), _stream()), "hg_op_apply")
-        return out.cpu().numpy() if was_np else out
+        if was_np:
+            res = out.cpu().numpy()
+            self.precond.check()
+            return res
+        return out
 
     def basis(self, nv, col=0):
         """The first nv Krylov basis vectors of column col of the last GMRES
         solve on this operator, as an (nv, n) CUDA tensor (inspection hook)."""
         return _basis(self._handle, self.n, col, nv)
+
+    def release(self):
+        """Free this operator's Krylov bases / GMRES workspaces (hg_op_release)."""
+        _lib.check(_lib.load().hg_op_release(self._handle), "hg_op_release")
 
     def apply_multi(self, V):
         """op applied to every column of a batch (numpy (n, nrhs) or CUDA (nrhs, n))."""
@@ -565,7 +587,10 @@ class DeviceOperator:
             _lib.load().hg_op_apply_multi(self._handle, _vp(t), self.n, _vp(out), self.n, t.shape[0], _stream()),
             "hg_op_apply_multi",
         )
-        return _from_device_batch(out, was_np)
+        res = _from_device_batch(out, was_np)
+        if was_np:
+            self.precond.check()
+        return res
 
     def __del__(self):
         try:
@@ -618,6 +643,10 @@ class CsrOperator:
         """The first nv Krylov basis vectors of column col of the last GMRES
         solve on this operator, as an (nv, n) CUDA tensor (inspection hook)."""
         return _basis(self._handle, self.n, col, nv)
+
+    def release(self):
+        """Free this operator's Krylov bases / GMRES workspaces (hg_op_release)."""
+        _lib.check(_lib.load().hg_op_release(self._handle), "hg_op_release")
 
     def apply_multi(self, V):
         """op applied to every column of a batch (numpy (n, nrhs) or CUDA (nrhs, n))."""
