@@ -16,6 +16,7 @@ no CPU path: without the library or a GPU the calls raise.
 
 import ctypes
 import os
+import types
 from dataclasses import dataclass
 
 import numpy as np
@@ -122,18 +123,21 @@ class LocalSolver:
     """Mirror of schwarz.LocalSolver (schwarz.py:26-34); ``min_eig`` and
     ``spd_flag`` are computed lazily (they only feed reports)."""
 
-    def __init__(self, coarse_index, fine_index, idof, lu, diameter, block):
+    def __init__(self, coarse_index, fine_index, idof, lu, diameter, block, matrix=None):
         self.coarse_index = coarse_index
         self.fine_index = fine_index
         self.idof = idof
         self.lu = lu
         self.diameter = diameter
         self._block = block
+        self._matrix = matrix  # global B, to cut the block on demand (cached handles)
         self._min_eig = None
 
     @property
     def min_eig(self):
         if self._min_eig is None:
+            if self._block is None and self.idof.size:
+                self._block = submatrix(self._matrix, self.idof, self.idof)
             self._min_eig = _smallest_eigenvalue(self._block) if self.idof.size else np.inf
         return self._min_eig
 
@@ -205,7 +209,9 @@ def coarse_blocks(coarse, dec):
 class TwoLevelPreconditioner:
     """Device-resident M^{-1} r = Z B0^{-1} Z^T r + sum_s E_s B_s^{-1} R_s r."""
 
-    def __init__(self, forms, dec, coarse=None, b0_lu=None):
+    def __init__(self, forms, dec, coarse=None, b0_lu=None, keep_image=False):
+        self._keep_image = keep_image
+        self._image_arrays = None
         self.forms = forms
         self.n = forms.n_dofs if hasattr(forms, "n_dofs") else forms.helmholtz.shape[0]
         self._handle = None
@@ -252,23 +258,62 @@ class TwoLevelPreconditioner:
 
     # ------------------------------------------------------------------ upload
     def _upload(self, B, Dk, factors, cblocks, lu, piv):
-        keep = self._keep
-        lib = _lib.load()
-        _torch()  # CUDA context present before the first allocation
-        d = _lib.HgPrecondDesc()
-        i32, i64, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+        arrays, meta = self._image(B, Dk, factors, cblocks, lu, piv)
+        meta["labels"] = [[int(ls.coarse_index), int(ls.fine_index)] for ls in self.local_solvers]
+        if self._keep_image:
+            self._image_arrays = arrays
+            self._meta = meta
+        if not getattr(self, "_host_only", False):
+            self._create(arrays, meta)
 
-        def arr(a, dtype, ctype):
-            a = np.ascontiguousarray(a, dtype=dtype)
-            keep.append(a)
-            return _lib.ptr(a, ctype)
+    @classmethod
+    def from_image(cls, arrays, meta, forms=None):
+        """A preconditioner straight from an image (the on-disk setup cache,
+        cache.py): hg_precond_create on the stored arrays, no host setup."""
+        from .cache import forms_from_image
 
-        d.n = self.n
-        d.nnz = B.nnz
-        d.indptr = arr(B.indptr, np.int32, i32)
-        d.indices = arr(B.indices, np.int32, i32)
-        d.b_data = arr(B.data, np.float64, f64)
-        d.dk_data = arr(Dk.data, np.float64, f64) if Dk is not None else None
+        self = cls.__new__(cls)
+        self._keep_image = True
+        self._image_arrays = arrays
+        self.forms = forms if forms is not None else forms_from_image(arrays, meta)
+        self.n = int(meta["n"])
+        self._handle = None
+        self._keep = []
+        self.Z = None
+        self.b0_piv = None
+        self._B = self.forms.helmholtz
+        self._Dk = self.forms.dk
+        self._create(arrays, meta)
+        off = np.asarray(arrays["local_idx_off"])
+        idx = arrays["local_idx"]
+        self.local_solvers = []
+        for s, (ci, fi) in enumerate(meta["labels"]):
+            idof = np.asarray(idx[off[s]:off[s + 1]], dtype=np.int64)
+            kl, kv = meta["local_bands"][s]
+            ls = LocalSolver(ci, fi, idof, None, np.nan, None, matrix=self._B)
+            ls.lu = GpuBandLU(self, s, types.SimpleNamespace(n=int(idof.size), kl=kl, kv=kv))
+            self.local_solvers.append(ls)
+        return self
+
+    def _image(self, B, Dk, factors, cblocks, lu, piv):
+        """Everything hg_precond_create consumes, as host arrays (named after
+        the HgPrecondDesc fields) plus scalars: the unit the on-disk setup
+        cache (cache.py) stores."""
+        A, M = {}, {}
+        i32, i64, f64 = np.int32, np.int64, np.float64
+
+        def put(name, a, dtype):
+            A[name] = np.ascontiguousarray(a, dtype=dtype)
+
+        M["n"] = int(self.n)
+        M["nnz"] = int(B.nnz)
+        k = getattr(self.forms, "k", None)
+        M["k"] = None if k is None else float(k)
+        put("indptr", B.indptr, i32)
+        put("indices", B.indices, i32)
+        put("b_data", B.data, f64)
+        if Dk is not None:
+            put("dk_data", Dk.data, f64)
 
         ns, kls, kvs, fss, bss = [], [], [], [], []
         idx_off = [0]
@@ -290,29 +335,28 @@ class TwoLevelPreconditioner:
             bwd_parts.append(bw.ravel())
             fpos += fw.size
             bpos += bw.size
-        fwd = np.concatenate(fwd_parts) if fwd_parts else np.zeros(0)
-        bwd = np.concatenate(bwd_parts) if bwd_parts else np.zeros(0)
-        d.n_local = len(factors)
-        d.local_n = arr(ns, np.int32, i32)
-        d.local_kl = arr(kls, np.int32, i32)
-        d.local_kv = arr(kvs, np.int32, i32)
-        d.local_fstride = arr(fss, np.int32, i32)
-        d.local_bstride = arr(bss, np.int32, i32)
-        d.local_idx_off = arr(idx_off, np.int64, i64)
-        d.local_idx = arr(np.concatenate([i for i, _ in factors]) if factors else np.zeros(0), np.int32, i32)
-        d.local_fwd_off = arr(foff, np.int64, i64)
-        d.local_fwd_len = fwd.size
-        d.local_fwd = arr(fwd, np.float64, f64)
-        d.local_bwd_off = arr(boff, np.int64, i64)
-        d.local_bwd_len = bwd.size
-        d.local_bwd = arr(bwd, np.float64, f64)
+        M["n_local"] = len(factors)
+        put("local_n", ns, i32)
+        put("local_kl", kls, i32)
+        put("local_kv", kvs, i32)
+        put("local_fstride", fss, i32)
+        put("local_bstride", bss, i32)
+        put("local_idx_off", idx_off, i64)
+        put("local_idx", np.concatenate([i for i, _ in factors]) if factors else np.zeros(0), i32)
+        put("local_fwd_off", foff, i64)
+        put("local_fwd", np.concatenate(fwd_parts) if fwd_parts else np.zeros(0), f64)
+        put("local_bwd_off", boff, i64)
+        put("local_bwd", np.concatenate(bwd_parts) if bwd_parts else np.zeros(0), f64)
+        M["local_fwd_len"] = int(A["local_fwd"].size)
+        M["local_bwd_len"] = int(A["local_bwd"].size)
+        M["local_bands"] = [[int(f.kl), int(f.kv)] for _, f in factors]
 
         m = sum(b.shape[1] for _, b in cblocks)
-        d.m = m
-        self.m = m
-        self.local_sizes = ns
-        self.cblock_shapes = [b.shape for _, b in cblocks]
-        self.b0_bytes = 0
+        M["m"] = int(m)
+        M["cblock_shapes"] = [[int(b.shape[0]), int(b.shape[1])] for _, b in cblocks]
+        M["b0_bytes"] = 0
+        M["b0_mode"] = -1
+        M["b0_dense"] = False
         if m:
             P = int(os.environ.get("HG_B0_PANEL", "64"))
             T = pack_b0_tiles(lu, piv, P)
@@ -324,21 +368,24 @@ class TwoLevelPreconditioner:
                 mode = 0
             if mode == 1:
                 T = T.premultiply()  # tiles D_t^{-1} T[t, j]: rows of a panel finish independently
-            # guard: the tiled algorithm (inverted diagonal blocks) must agree with getrs
-            c = np.random.default_rng(0).standard_normal(m)
-            want = scipy.linalg.lu_solve((lu, piv), c)
-            dev = float(np.abs(T.solve(c) - want).max() / max(np.abs(want).max(), 1e-300))
+            # guard: the tiled algorithm (inverted diagonal blocks) must agree with getrs on several
+            # vectors (a getrs-equivalent operator: explicit inverses of 64x64 blocks)
+            rng = np.random.default_rng(0)
+            dev = 0.0
+            for _ in range(4):
+                c = rng.standard_normal(m)
+                want = scipy.linalg.lu_solve((lu, piv), c)
+                dev = max(dev, float(np.abs(T.solve(c) - want).max() / max(np.abs(want).max(), 1e-300)))
             if dev > 1e-11:
                 raise SingularOperatorError(
                     "coarse tile factorisation deviates from getrs by %.2e (B0 too ill-conditioned for "
                     "inverted %dx%d diagonal blocks)" % (dev, P, P))
             self.b0_tiles = T
-            self.b0_tile_dev = dev
-            self.b0_bytes = T.nbytes + 4 * m + 4 * T.tile_col.size
+            M["b0_tile_dev"] = dev
+            M["b0_bytes"] = int(T.nbytes + 4 * m + 4 * T.tile_col.size)
             # dense mode: B0^{-1} applied as a streaming GEMV / DMMA GEMM beside the
             # local solves; kept only if it agrees with getrs (the reference's lu_solve)
-            self.b0_dense = False
-            self.b0_dense_dev = None
+            M["b0_dense_dev"] = None
             dense = os.environ.get("HG_B0_DENSE", "0")  # measured slower by default: see DESIGN.md section 8
             if dense == "1" or (dense == "auto" and m <= 20000):  # "auto": whenever it fits
                 torch = _torch()
@@ -351,48 +398,68 @@ class TwoLevelPreconditioner:
                     c = rng.standard_normal(m)
                     want = scipy.linalg.lu_solve((lu, piv), c)
                     ddev = max(ddev, float(np.abs(Binv @ c - want).max() / max(np.abs(want).max(), 1e-300)))
-                self.b0_dense_dev = ddev
+                M["b0_dense_dev"] = ddev
                 if ddev <= 1e-11:
-                    self.b0_dense = True
-                    d.b0_inv = arr(Binv, np.float64, f64)
-                    self.b0_bytes = 8 * m * m + 16 * m
-            d.n_cblk = len(cblocks)
-            d.cblk_n = arr([i.size for i, _ in cblocks], np.int32, i32)
-            d.cblk_m = arr([b.shape[1] for _, b in cblocks], np.int32, i32)
-            d.cblk_idx_off = arr(np.concatenate([[0], np.cumsum([i.size for i, _ in cblocks])]), np.int64, i64)
-            d.cblk_idx = arr(np.concatenate([i for i, _ in cblocks]), np.int32, i32)
+                    M["b0_dense"] = True
+                    put("b0_inv", Binv, f64)
+                    M["b0_bytes"] = int(8 * m * m + 16 * m)
+            M["n_cblk"] = len(cblocks)
+            put("cblk_n", [i.size for i, _ in cblocks], i32)
+            put("cblk_m", [b.shape[1] for _, b in cblocks], i32)
+            put("cblk_idx_off", np.concatenate([[0], np.cumsum([i.size for i, _ in cblocks])]), i64)
+            put("cblk_idx", np.concatenate([i for i, _ in cblocks]), i32)
             zsizes = [b.size for _, b in cblocks]
-            d.cblk_z_off = arr(np.concatenate([[0], np.cumsum(zsizes)[:-1]]), np.int64, i64)
-            z = np.concatenate([b.ravel() for _, b in cblocks])
-            d.z_len = z.size
-            d.z_data = arr(z, np.float64, f64)
-            d.b0_perm = arr(T.perm, np.int32, i32)
-            d.b0_panel = T.P
-            d.b0_npanel = T.K
-            d.b0_tile_ptr = arr(T.tile_ptr, np.int64, i64)
-            d.b0_tile_col = arr(T.tile_col if T.tile_col.size else np.zeros(1), np.int32, i32)
-            d.b0_ntile = int(T.tile_col.size)
-            d.b0_ctas = int(os.environ.get("HG_B0_CTAS", "0"))
-            self.b0_mode = mode
+            put("cblk_z_off", np.concatenate([[0], np.cumsum(zsizes)[:-1]]), i64)
+            put("z_data", np.concatenate([b.ravel() for _, b in cblocks]), f64)
+            M["z_len"] = int(A["z_data"].size)
+            put("b0_perm", T.perm, i32)
+            M["b0_panel"] = int(T.P)
+            M["b0_npanel"] = int(T.K)
+            put("b0_tile_ptr", T.tile_ptr, i64)
+            put("b0_tile_col", T.tile_col if T.tile_col.size else np.zeros(1), i32)
+            M["b0_ntile"] = int(T.tile_col.size)
+            M["b0_ctas"] = int(os.environ.get("HG_B0_CTAS", "0"))
+            M["b0_mode"] = mode
             if mode == 1:
-                d.b0_mode, d.b0_cluster, d.b0_ring = 1, cs, ring
+                M["b0_cluster"], M["b0_ring"] = int(cs), int(ring)
                 dinv = swizzle_tile_rows(T.dinv)
                 tiles = swizzle_tile_rows(T.tiles) if T.tiles.size else np.zeros(1)
             else:
-                d.b0_mode, d.b0_cluster, d.b0_ring = 0, 0, 0
+                M["b0_cluster"], M["b0_ring"] = 0, 0
                 dinv, tiles = T.dinv, (T.tiles if T.tiles.size else np.zeros(1))
-            d.b0_dinv = arr(dinv, np.float64, f64)
-            d.b0_tiles = arr(tiles, np.float64, f64)
+            put("b0_dinv", dinv, f64)
+            put("b0_tiles", tiles, f64)
+        return A, M
+
+    def _create(self, arrays, meta):
+        """hg_precond_create from an image (``_image`` or the setup cache)."""
+        lib = _lib.load()
+        _torch()  # CUDA context present before the first allocation
+        d = _lib.HgPrecondDesc()
+        for name, ctype in _lib.HgPrecondDesc._fields_:
+            if issubclass(ctype, ctypes._Pointer):  # array field
+                a = arrays.get(name)
+                setattr(d, name, None if a is None else a.ctypes.data_as(ctype))
+            else:
+                setattr(d, name, int(meta.get(name, 0)))
         h = ctypes.c_void_p()
         _lib.check(lib.hg_precond_create(ctypes.byref(d), ctypes.byref(h)), "hg_precond_create")
         self._handle = h
-        self._keep = []  # host copies no longer needed
-        self.local_bands = [(f.kl, f.kv) for _, f in factors]
+        self._meta = meta
+        self.m = int(meta["m"])
+        self.local_sizes = [int(x) for x in arrays["local_n"]] if "local_n" in arrays else []
+        self.local_bands = [tuple(b) for b in meta["local_bands"]]
+        self.cblock_shapes = [tuple(c) for c in meta["cblock_shapes"]]
+        self.b0_bytes = int(meta["b0_bytes"])
+        self.b0_mode = int(meta["b0_mode"])
+        self.b0_dense = bool(meta["b0_dense"])
+        self.b0_dense_dev = meta.get("b0_dense_dev")
+        self.b0_tile_dev = meta.get("b0_tile_dev")
 
     # ------------------------------------------------------------------ API
     @property
     def has_coarse(self):
-        return self.b0_piv is not None
+        return self.m > 0
 
     @property
     def device_bytes(self):
@@ -668,6 +735,18 @@ class CsrOperator:
             pass
 
 
-def factorize(forms, dec, coarse=None):
-    """GPU ``factorize`` (schwarz.py:74-101): host factorisations + upload."""
-    return TwoLevelPreconditioner(forms, dec, coarse)
+def host_image(forms, dec, coarse=None):
+    """(arrays, meta) of the device image the GPU factorize would upload,
+    computed on the host only (no device, no handle): the cache format's
+    contents (cache.save_image), testable without a GPU."""
+    pre = TwoLevelPreconditioner.__new__(TwoLevelPreconditioner)
+    pre._host_only = True
+    TwoLevelPreconditioner.__init__(pre, forms, dec, coarse, keep_image=True)
+    return pre._image_arrays, pre._meta
+
+
+def factorize(forms, dec, coarse=None, keep_image=False):
+    """GPU ``factorize`` (schwarz.py:74-101): host factorisations + upload.
+    ``keep_image``: keep the uploaded host arrays so that
+    cache.save_preconditioner can write them (the on-disk setup cache)."""
+    return TwoLevelPreconditioner(forms, dec, coarse, keep_image=keep_image)
