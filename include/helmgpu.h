@@ -156,6 +156,27 @@ typedef struct {
    * against getrs (factorize does, bar 1e-11) — same operator, different
    * rounding. */
   const double* b0_inv;
+
+  /* Device factorisation of the local blocks.  When
+   * local_fwd and local_bwd are NULL, hg_precond_create builds the records
+   * itself: block s is given as a block-local CSR (its rows at
+   * lcsr_indptr[local_idx_off[s] + s .. + n_s], absolute offsets into
+   * lcsr_cols / lcsr_vals; columns block-local, ascending) with band
+   * half-width local_bw[s] (kl = ku), and is factored on the device with
+   * LAPACK dgbtrf semantics (partial pivoting within the band, multipliers
+   * by the reciprocal pivot; schwarz.py:104-131 _factor_block) straight into
+   * the record layout above (local_kl / local_kv / strides / offsets still
+   * describe it; local_fwd_len / local_bwd_len size it).  factor_info[s]
+   * (host out) receives dgbtrf's INFO (0, or j+1 for the first exactly-zero
+   * pivot) and factor_min_pivot[s] (host out) min_j |u_jj|, for the
+   * caller's singular-block test.  hg_precond_read returns the records. */
+  const int32_t* local_bw;
+  const int64_t* lcsr_indptr;
+  const int32_t* lcsr_cols;
+  const double* lcsr_vals;
+  int64_t lcsr_nnz;
+  int32_t* factor_info;
+  double* factor_min_pivot;
 } HgPrecondDesc;
 
 /* ---- library ---- */
@@ -183,6 +204,13 @@ int hg_precond_status(HgPrecond* p);
 int hg_precond_destroy(HgPrecond* p);
 /* device bytes held by the handle */
 int64_t hg_precond_device_bytes(const HgPrecond* p);
+/* Copy a device-resident array of the handle to host memory (e.g. the
+ * records of a device factorisation, for the on-disk setup cache):
+ * field HG_FIELD_LOCAL_FWD / HG_FIELD_LOCAL_BWD, `count` doubles (the
+ * desc's local_fwd_len / local_bwd_len). */
+#define HG_FIELD_LOCAL_FWD 1
+#define HG_FIELD_LOCAL_BWD 2
+int hg_precond_read(HgPrecond* p, int32_t field, double* host, int64_t count);
 /* out = M^{-1} r ; r, out: device, length n; out fully overwritten. */
 int hg_precond_apply(HgPrecond* p, const double* r, double* out, void* stream);
 /* out = M^{-1} (B u) */

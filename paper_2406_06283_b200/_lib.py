@@ -63,6 +63,13 @@ class HgPrecondDesc(ctypes.Structure):
         ("b0_cluster", ctypes.c_int32),
         ("b0_ring", ctypes.c_int32),
         ("b0_inv", _f64p),
+        ("local_bw", _i32p),
+        ("lcsr_indptr", _i64p),
+        ("lcsr_cols", _i32p),
+        ("lcsr_vals", _f64p),
+        ("lcsr_nnz", ctypes.c_int64),
+        ("factor_info", _i32p),
+        ("factor_min_pivot", _f64p),
     ]
 
 
@@ -118,7 +125,9 @@ SIGNATURES = {
     "hg_op_release": (ctypes.c_int, [_vp]),
     "hg_dcgs2_explicit_passes": (ctypes.c_int64, []),
     "hg_debug_set": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int64]),
+    "hg_precond_read": (ctypes.c_int, [_vp, ctypes.c_int32, _f64p, ctypes.c_int64]),
 }
+FIELD_LOCAL_FWD, FIELD_LOCAL_BWD = 1, 2
 
 ABI_VERSION = 3
 DEBUG_SPIN_LIMIT_MS, DEBUG_SKIP_ZT, DEBUG_FORCE_EXPLICIT_RHO = 1, 2, 3

@@ -818,6 +818,68 @@ static int build_contrib(int n, int nblk, const int64_t* off, const int32_t* idx
   return HG_OK;
 }
 
+// Device factorisation of the local blocks (desc without records): band LU
+// straight into the zeroed record arrays (hg_factor.cu), INFO and the
+// smallest pivot per block back to the caller.
+static int device_factor_local(HgPrecond* P, const HgPrecondDesc* D) {
+  if (!D->local_bw || !D->lcsr_indptr || !D->lcsr_cols || !D->lcsr_vals || !D->factor_info ||
+      !D->factor_min_pivot) {
+    set_error("hg_precond_create: no local records and no block CSR to factor");
+    return HG_ERR_ARG;
+  }
+  const int nl = D->n_local;
+  int kl_max = 0;
+  for (int s = 0; s < nl; ++s) kl_max = std::max(kl_max, (int)D->local_bw[s]);
+  for (int s = 0; s < nl; ++s) {
+    const LocalDesc& d = P->h_local[s];
+    if (d.kl < D->local_bw[s] || d.kv < 2 * D->local_bw[s]) {
+      set_error("hg_precond_create: record widths narrower than the band of block " + std::to_string(s));
+      return HG_ERR_ARG;
+    }
+  }
+  if (!band_lu_supported(kl_max, kl_max)) {
+    set_error("hg_precond_create: device band LU supports half-widths <= 79 (got " + std::to_string(kl_max) +
+              "); pass host records");
+    return HG_ERR_UNSUPPORTED;
+  }
+  HG_CUDA_TRY(cudaMemset(P->d_fwd, 0, sizeof(double) * (size_t)D->local_fwd_len));
+  HG_CUDA_TRY(cudaMemset(P->d_bwd, 0, sizeof(double) * (size_t)D->local_bwd_len));
+  std::vector<long long> base(nl);
+  for (int s = 0; s < nl; ++s) base[s] = (long long)D->local_idx_off[s] + s;
+  const long long nptr = (long long)D->local_idx_off[nl] + nl;
+  int *d_bw = nullptr, *d_cols = nullptr, *d_info = nullptr;
+  long long *d_base = nullptr, *d_ip = nullptr;
+  double *d_vals = nullptr, *d_minp = nullptr;
+  int s = HG_OK;
+  if ((s = upload(&d_bw, D->local_bw, (size_t)nl, nullptr)) == HG_OK &&
+      (s = upload(&d_base, base.data(), (size_t)nl, nullptr)) == HG_OK &&
+      (s = upload(&d_ip, reinterpret_cast<const long long*>(D->lcsr_indptr), (size_t)nptr, nullptr)) == HG_OK &&
+      (s = upload(&d_cols, D->lcsr_cols, (size_t)D->lcsr_nnz, nullptr)) == HG_OK &&
+      (s = upload(&d_vals, D->lcsr_vals, (size_t)D->lcsr_nnz, nullptr)) == HG_OK &&
+      (s = upload<int>(&d_info, nullptr, (size_t)nl, nullptr)) == HG_OK &&
+      (s = upload<double>(&d_minp, nullptr, (size_t)nl, nullptr)) == HG_OK) {
+    s = launch_band_lu(P, d_bw, kl_max, kl_max, d_base, d_ip, d_cols, d_vals, d_info, d_minp, 0);
+    if (s == HG_OK && cudaDeviceSynchronize() != cudaSuccess) {
+      set_error(std::string("device band LU: ") + cudaGetErrorString(cudaGetLastError()));
+      s = HG_ERR_CUDA;
+    }
+    if (s == HG_OK && (cudaMemcpy(D->factor_info, d_info, sizeof(int) * nl, cudaMemcpyDeviceToHost) != cudaSuccess ||
+                       cudaMemcpy(D->factor_min_pivot, d_minp, sizeof(double) * nl, cudaMemcpyDeviceToHost) !=
+                           cudaSuccess)) {
+      set_error("device band LU: reading INFO back failed");
+      s = HG_ERR_CUDA;
+    }
+  }
+  release(d_bw);
+  release(d_base);
+  release(d_ip);
+  release(d_cols);
+  release(d_vals);
+  release(d_info);
+  release(d_minp);
+  return s;
+}
+
 static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
   long long* bytes = &P->device_bytes;
   const int n = D->n;
@@ -885,10 +947,13 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
   if (D->n_local > 0) {
     const long long nidx = D->local_idx_off[D->n_local];
     P->xs_len = nidx;
+    P->fwd_len = D->local_fwd_len;
+    P->bwd_len = D->local_bwd_len;
     HG_TRY(upload(&P->d_local, P->h_local.data(), P->h_local.size(), bytes));
     HG_TRY(upload(&P->d_local_idx, D->local_idx, (size_t)nidx, bytes));
     HG_TRY(upload(&P->d_fwd, D->local_fwd, (size_t)D->local_fwd_len, bytes));
     HG_TRY(upload(&P->d_bwd, D->local_bwd, (size_t)D->local_bwd_len, bytes));
+    if (!D->local_fwd || !D->local_bwd) HG_TRY(device_factor_local(P, D));
     HG_TRY(upload<double>(&P->d_xs, nullptr, (size_t)nidx, bytes));
     std::vector<int> ptr;
     std::vector<long long> ent;
@@ -1017,6 +1082,31 @@ int hg_precond_create(const HgPrecondDesc* desc, HgPrecond** out) {
 }
 
 int64_t hg_precond_device_bytes(const HgPrecond* P) { return P ? P->device_bytes : 0; }
+
+int hg_precond_read(HgPrecond* P, int32_t field, double* host, int64_t count) {
+  if (!P || !host || count < 0) {
+    set_error("hg_precond_read: bad argument");
+    return HG_ERR_ARG;
+  }
+  const double* src = nullptr;
+  long long len = 0;
+  if (field == HG_FIELD_LOCAL_FWD) {
+    src = P->d_fwd;
+    len = P->fwd_len;
+  } else if (field == HG_FIELD_LOCAL_BWD) {
+    src = P->d_bwd;
+    len = P->bwd_len;
+  } else {
+    set_error("hg_precond_read: unknown field");
+    return HG_ERR_ARG;
+  }
+  if (count != len) {
+    set_error("hg_precond_read: count " + std::to_string(count) + " != field length " + std::to_string(len));
+    return HG_ERR_ARG;
+  }
+  if (len) HG_CUDA_TRY(cudaMemcpy(host, src, sizeof(double) * (size_t)len, cudaMemcpyDeviceToHost));
+  return HG_OK;
+}
 
 int hg_precond_apply(HgPrecond* P, const double* r, double* out, void* stream) {
   if (!P || !r || !out) {

@@ -45,6 +45,7 @@ struct HgPrecond {
   int* d_local_idx = nullptr;
   double* d_fwd = nullptr;
   double* d_bwd = nullptr;
+  long long fwd_len = 0, bwd_len = 0;
   long long xs_len = 0;
   double* d_xs = nullptr;         // per-block local solutions (scratch)
   // dof -> local contributions (positions in xs), fixed (subdomain) order
@@ -169,6 +170,11 @@ int launch_local_solve_multi(HgPrecond* P, const double* R, long long ldr, int n
 int launch_local_blocked(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st);
 int preload_local_blocked();
 int launch_local_solve_single(HgPrecond* P, int s, const double* r_local, double* x_local, cudaStream_t st);
+// device band LU of every local block into P->d_fwd / P->d_bwd (hg_factor.cu)
+int band_lu_supported(int kl_max, int ku_max);
+int launch_band_lu(HgPrecond* P, const int* d_bw, int kl_max, int ku_max, const long long* d_ptr_base,
+                   const long long* d_indptr, const int* d_cols, const double* d_vals, int* d_info, double* d_minpiv,
+                   cudaStream_t st);
 int launch_zt(HgPrecond* P, const double* r, cudaStream_t st);
 // zt_target: value of the Z^T r chunk counter the solve waits for before reading c
 // the solve waits (bounded, device side) for the Z^T r launch it pairs with

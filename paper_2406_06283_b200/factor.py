@@ -127,6 +127,13 @@ def record_floor(kw_max):
     return max(0, 32 * register_tiles(kw_max) - 65)
 
 
+def record_widths(kl, kv, kl_floor=0, kv_floor=0):
+    """(fstride, bstride, kl_rec, kv_rec) of one block's records (as
+    pack_band_records lays them out)."""
+    klp, kvp = max(kl, MIN_RECORD_WIDTH, kl_floor), max(kv, MIN_RECORD_WIDTH, kv_floor)
+    return _even(klp + 1), _even(kvp + 1), klp, kvp
+
+
 def pack_band_records(f, kl_floor=0, kv_floor=0):
     """(fwd records, bwd records, fstride, bstride, kl_rec, kv_rec) for one
     BandLU; widths below MIN_RECORD_WIDTH or the launch's record floors

@@ -25,10 +25,12 @@ import scipy.sparse as sp
 
 from . import _lib
 from .errors import SingularOperatorError
-from .factor import (band_lu, lu_b0, pack_b0_tiles, pack_band_records, record_floor, submatrix, swizzle_tile_rows,
-                     tile_span)
+from .factor import (BandLU, band_lu, block_bandwidth, lu_b0, pack_b0_tiles, pack_band_records, record_floor,
+                     record_widths, submatrix, swizzle_tile_rows, tile_span)
 
 _DENSE_EIG_LIMIT = 1500
+_SINGULAR_RTOL = 1e-12
+DEVICE_BAND_MAX = 79  # widest band half-width the device band LU compiles (hg_factor.cu windows)
 
 
 def _torch():
@@ -101,13 +103,21 @@ def _from_device_batch(t, was_np):
 
 class GpuBandLU:
     """``LocalSolver.lu`` stand-in: ``solve`` runs the device band solve of
-    one block (hg_local_solve); the host factors stay available for tests."""
+    one block (hg_local_solve).  ``host`` = the host dgbtrf factors of the
+    block (computed on first access when the device factorised it; tests)."""
 
     def __init__(self, precond, index, host_factor):
         self._p = precond
         self._s = index
-        self.host = host_factor
+        self._host = host_factor if isinstance(host_factor, BandLU) else None
         self.shape = (host_factor.n, host_factor.n)
+
+    @property
+    def host(self):
+        if self._host is None:
+            ls = self._p.local_solvers[self._s]
+            self._host = band_lu(submatrix(self._p._B, ls.idof, ls.idof), label=(ls.coarse_index, ls.fine_index))
+        return self._host
 
     def solve(self, rhs):
         torch = _torch()
@@ -228,18 +238,30 @@ class TwoLevelPreconditioner:
         self._B = B
         self._Dk = Dk
 
-        # ---- local factorisations (schwarz.py:83-85, 104-131)
+        # ---- local factorisations (schwarz.py:83-85, 104-131): on the device
+        # (hg_factor.cu, dgbtrf semantics) unless a block's band is wider than
+        # the compiled windows or HG_HOST_FACTOR=1 asks for LAPACK dgbtrf here
         self.local_solvers = []
         factors = []
+        blocks = []
         for i, j, sub in dec.fine_flat():
             idof = np.asarray(sub.idof)
             block = submatrix(B, idof, idof) if idof.size else sp.csr_matrix((0, 0))
-            if idof.size:
-                f = band_lu(block, label=(i, j))
+            blocks.append(block)
+            self.local_solvers.append(LocalSolver(i, j, idof, None, getattr(sub, "diameter", np.nan), block,
+                                                  matrix=B))
+        bws = [block_bandwidth(b) if b.shape[0] else 0 for b in blocks]
+        self.device_factor = (os.environ.get("HG_HOST_FACTOR", "0") != "1" and not self._host_only_factor()
+                              and max(bws, default=0) <= DEVICE_BAND_MAX)
+        for ls, block, bw in zip(self.local_solvers, blocks, bws):
+            if self.device_factor:
+                f = types.SimpleNamespace(n=block.shape[0], kl=bw, ku=bw, kv=2 * bw, block=block,
+                                          norm=float(np.sqrt(np.sum(block.data ** 2))) if block.nnz else 0.0)
+            elif block.shape[0]:
+                f = band_lu(block, label=(ls.coarse_index, ls.fine_index))
             else:
                 f = band_lu(sp.csr_matrix((0, 0)))
-            factors.append((idof, f))
-            self.local_solvers.append(LocalSolver(i, j, idof, None, getattr(sub, "diameter", np.nan), block))
+            factors.append((ls.idof, f))
 
         # ---- coarse operator (schwarz.py:87-100)
         cblocks = []
@@ -256,15 +278,50 @@ class TwoLevelPreconditioner:
         for s, ls in enumerate(self.local_solvers):
             ls.lu = GpuBandLU(self, s, factors[s][1])
 
+    def _host_only_factor(self):
+        return getattr(self, "_host_only", False)  # host_image(): no device to factor on
+
     # ------------------------------------------------------------------ upload
     def _upload(self, B, Dk, factors, cblocks, lu, piv):
         arrays, meta = self._image(B, Dk, factors, cblocks, lu, piv)
         meta["labels"] = [[int(ls.coarse_index), int(ls.fine_index)] for ls in self.local_solvers]
+        if getattr(self, "_host_only", False):
+            self._image_arrays, self._meta = arrays, meta
+            return
+        self._create(arrays, meta)
+        if "factor_info" in arrays:
+            self._check_device_factor(arrays, meta)
+            if self._keep_image:  # the cache stores the device-built records, not the factor inputs
+                arrays = dict(arrays)
+                for field, name, length in ((_lib.FIELD_LOCAL_FWD, "local_fwd", meta["local_fwd_len"]),
+                                            (_lib.FIELD_LOCAL_BWD, "local_bwd", meta["local_bwd_len"])):
+                    buf = np.empty(int(length))
+                    _lib.check(_lib.load().hg_precond_read(self._handle, field, _lib.ptr(buf, ctypes.c_double),
+                                                           int(length)), "hg_precond_read")
+                    arrays[name] = buf
+                for name in ("local_bw", "lcsr_indptr", "lcsr_cols", "lcsr_vals", "factor_info", "factor_min_pivot"):
+                    arrays.pop(name, None)
+                meta = dict(meta)
+                meta.pop("lcsr_nnz", None)
         if self._keep_image:
             self._image_arrays = arrays
             self._meta = meta
-        if not getattr(self, "_host_only", False):
-            self._create(arrays, meta)
+
+    def _check_device_factor(self, arrays, meta):
+        """The singular-block test of schwarz.py:111-121 on the device factors:
+        an exactly-zero pivot (dgbtrf INFO) or min |u_jj| <= 1e-12 ||block||_F."""
+        info, minp = arrays["factor_info"], arrays["factor_min_pivot"]
+        for s, ls in enumerate(self.local_solvers):
+            if ls.idof.size == 0:
+                continue
+            where = "fine subdomain (%d, %d)" % (ls.coarse_index, ls.fine_index)
+            if info[s] > 0:
+                raise SingularOperatorError(
+                    "local Helmholtz block on %s is singular (k^2 equals a local Dirichlet eigenvalue): "
+                    "zero pivot at %d" % (where, info[s]))
+            if minp[s] <= _SINGULAR_RTOL * meta["local_norms"][s]:
+                raise SingularOperatorError(
+                    "local Helmholtz block on %s is numerically singular (smallest pivot %.3e)" % (where, minp[s]))
 
     @classmethod
     def from_image(cls, arrays, meta, forms=None):
@@ -321,8 +378,23 @@ class TwoLevelPreconditioner:
         fpos = bpos = 0
         kl_floor = record_floor(max([f.kl for _, f in factors], default=0))
         kv_floor = record_floor(max([f.kv for _, f in factors], default=0))
+        device = getattr(self, "device_factor", False)
+        lptr, lcols, lvals = [], [], []
+        nnz_pos = 0
         for idof, f in factors:
-            fw, bw, fs, bs, klp, kvp = pack_band_records(f, kl_floor, kv_floor)
+            if device:
+                fs, bs, klp, kvp = record_widths(f.kl, f.kv, kl_floor, kv_floor)
+                blk = f.block
+                lptr.append(blk.indptr.astype(np.int64) + nnz_pos)
+                lcols.append(blk.indices)
+                lvals.append(blk.data)
+                nnz_pos += blk.nnz
+                fsize, bsize = f.n * fs, f.n * bs
+            else:
+                fw, bw, fs, bs, klp, kvp = pack_band_records(f, kl_floor, kv_floor)
+                fwd_parts.append(fw.ravel())
+                bwd_parts.append(bw.ravel())
+                fsize, bsize = fw.size, bw.size
             ns.append(f.n)
             kls.append(klp)
             kvs.append(kvp)
@@ -331,10 +403,8 @@ class TwoLevelPreconditioner:
             idx_off.append(idx_off[-1] + idof.size)
             foff.append(fpos)
             boff.append(bpos)
-            fwd_parts.append(fw.ravel())
-            bwd_parts.append(bw.ravel())
-            fpos += fw.size
-            bpos += bw.size
+            fpos += fsize
+            bpos += bsize
         M["n_local"] = len(factors)
         put("local_n", ns, i32)
         put("local_kl", kls, i32)
@@ -344,11 +414,21 @@ class TwoLevelPreconditioner:
         put("local_idx_off", idx_off, i64)
         put("local_idx", np.concatenate([i for i, _ in factors]) if factors else np.zeros(0), i32)
         put("local_fwd_off", foff, i64)
-        put("local_fwd", np.concatenate(fwd_parts) if fwd_parts else np.zeros(0), f64)
         put("local_bwd_off", boff, i64)
-        put("local_bwd", np.concatenate(bwd_parts) if bwd_parts else np.zeros(0), f64)
-        M["local_fwd_len"] = int(A["local_fwd"].size)
-        M["local_bwd_len"] = int(A["local_bwd"].size)
+        M["local_fwd_len"] = int(fpos)
+        M["local_bwd_len"] = int(bpos)
+        if device:
+            put("local_bw", [f.kl for _, f in factors], i32)
+            put("lcsr_indptr", np.concatenate(lptr) if lptr else np.zeros(0), i64)
+            put("lcsr_cols", np.concatenate(lcols) if lcols else np.zeros(0), i32)
+            put("lcsr_vals", np.concatenate(lvals) if lvals else np.zeros(0), f64)
+            M["lcsr_nnz"] = int(nnz_pos)
+            put("factor_info", np.zeros(len(factors)), i32)
+            put("factor_min_pivot", np.zeros(len(factors)), f64)
+            M["local_norms"] = [float(f.norm) for _, f in factors]
+        else:
+            put("local_fwd", np.concatenate(fwd_parts) if fwd_parts else np.zeros(0), f64)
+            put("local_bwd", np.concatenate(bwd_parts) if bwd_parts else np.zeros(0), f64)
         M["local_bands"] = [[int(f.kl), int(f.kv)] for _, f in factors]
 
         m = sum(b.shape[1] for _, b in cblocks)
