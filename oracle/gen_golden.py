@@ -14,6 +14,9 @@ Files:
                 the one-level / degenerate cases) with applies on seeded r.
   wgmres.npz    reference weighted_gmres on the seeded random systems of
                 pkg/tests/test_wgmres.py.
+  analysis.npz  helmdd.analysis check_tf_stability / check_prop26_identity on
+                the setups of pkg/tests/test_analysis.py:300-323 and
+                check_t0_stability on the test_schwarz pipeline (n=16, k=10).
 """
 
 import os
@@ -135,12 +138,48 @@ def gen_wgmres(h):
     np.savez_compressed(os.path.join(OUT, "wgmres.npz"), **out)
 
 
+ANALYSIS_T0_THEORY = dict(k=10.0, lambda_overlap=1, theta=1e-6, cstab_estimate=1.0)
+
+
+def gen_analysis(h):
+    """helmdd.analysis lemma checks on the reference's own test setups
+    (test_analysis.py:300-323) plus a coarse-stability case with a theory
+    whose hypothesis holds (so every trial is asserted)."""
+    import types
+
+    from helmdd import analysis
+
+    out = {}
+
+    def store(tag, chk):
+        out[tag + "_trials"] = chk.trials
+        out[tag + "_violations"] = chk.violations
+        out[tag + "_worst"] = chk.worst_margin
+        out[tag + "_witness"] = chk.witness
+
+    mesh = h.build_unit_square_mesh(8)
+    space = h.build_fe_space(mesh)
+    forms = h.assemble_forms(mesh, space, h.coefficient_field(mesh), 0.5)
+    dec = h.build_two_level(mesh, space, 2, 2)
+    store("tf", analysis.check_tf_stability(forms, dec, h.factorize(forms, dec, None), trials=10,
+                                            rng=np.random.default_rng(5)))
+    forms = h.assemble_forms(mesh, space, h.coefficient_field(mesh), 5.0)
+    store("prop26", analysis.check_prop26_identity(forms, h.factorize(forms, dec, None), trials=20,
+                                                   rng=np.random.default_rng(6)))
+    forms, dec, coarse = _pipeline(h, 16, 2, 2, 10.0)
+    theory = types.SimpleNamespace(**ANALYSIS_T0_THEORY)
+    store("t0", analysis.check_t0_stability(forms, coarse, h.factorize(forms, dec, coarse), theory, trials=20,
+                                            rng=np.random.default_rng(7)))
+    np.savez_compressed(os.path.join(OUT, "analysis.npz"), **out)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     h = _ref()
     gen_small(h)
     gen_wgmres(h)
     gen_config1(h)
+    gen_analysis(h)
     print("golden vectors written to", OUT)
 
 

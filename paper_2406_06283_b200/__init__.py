@@ -58,6 +58,6 @@ from .schwarz import (
     factorize,
 )
 from .wgmres import GmresReport, elman_gamma, weighted_gmres, weighted_gmres_batch
-from .analysis import fov_bounds
+from .analysis import CheckReport, check_prop26_identity, check_t0_stability, check_tf_stability, fov_bounds
 
 __version__ = "0.1.0"

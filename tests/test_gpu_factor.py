@@ -76,7 +76,8 @@ def test_device_band_lu_matches_dgbtrf_configs_2_3(name, monkeypatch):
     host = hg.factorize(P.forms, P.dec, None, keep_image=True)
     piv_diff, wl, wu, swaps = compare_records(dev, host)
     assert piv_diff == 0 and wl <= 1e-11 and wu <= 1e-11, (piv_diff, wl, wu)
-    assert swaps > 0  # partial pivoting exercised (pivots occur at k = 40)
+    if name == "2":
+        assert swaps > 0  # partial pivoting exercised (pivots occur at k = 40, constant coefficient)
     r = np.random.default_rng(1).standard_normal(dev.n)
     assert rel(dev.apply(r), host.apply(r)) <= 1e-11
 
