@@ -211,6 +211,17 @@ int64_t hg_precond_device_bytes(const HgPrecond* p);
 #define HG_FIELD_LOCAL_FWD 1
 #define HG_FIELD_LOCAL_BWD 2
 int hg_precond_read(HgPrecond* p, int32_t field, double* host, int64_t count);
+/* Numbers about a handle (no synchronisation; NAN for an unknown key):
+ *   HG_STAT_PANEL_ACTIVE     1 if batched applies run the 16-row panel local
+ *                            solve (DMMA; built at create from the band
+ *                            records, HG_LOCAL_PANEL=0 disables), else 0
+ *   HG_STAT_PANEL_DEVIATION  its check against the row solve on a seeded
+ *                            16-column batch: max over columns of
+ *                            max|x_panel - x_row| / max|x_row| (must be
+ *                            <= 1e-11 to be active; -1 = not built) */
+#define HG_STAT_PANEL_ACTIVE 1
+#define HG_STAT_PANEL_DEVIATION 2
+double hg_precond_stat(HgPrecond* p, int32_t key);
 /* out = M^{-1} r ; r, out: device, length n; out fully overwritten. */
 int hg_precond_apply(HgPrecond* p, const double* r, double* out, void* stream);
 /* out = M^{-1} (B u) */

@@ -631,7 +631,7 @@ static int precond_apply_multi_core_impl(HgPrecond* P, const double* R, long lon
     HG_CUDA_TRY(cudaEventRecord(P->ev_join, P->aux));
     if (!ser) HG_TRY(launch_zt_multi(P, R, ldr, nrhs, st));
   }
-  HG_TRY(launch_local_solve_multi(P, R, ldr, nrhs, st));
+  HG_TRY(launch_local_batch(P, R, ldr, nrhs, st));
   if (P->m > 0) HG_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_join, 0));
   return launch_assemble_multi(P, true, true, OUT, ldo, nrhs, st);
 }
@@ -751,6 +751,9 @@ int hg_precond_destroy(HgPrecond* P) {
   release(P->d_local_idx);
   release(P->d_fwd);
   release(P->d_bwd);
+  release(P->d_poff);
+  release(P->d_pfwd);
+  release(P->d_pbwd);
   release(P->d_xs);
   release(P->d_lptr);
   release(P->d_lent);
@@ -1062,6 +1065,11 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
   HG_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
   HG_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
   HG_CUDA_TRY(cudaDeviceSynchronize());
+  if (P->n_local > 0) {  // batched solves on 16-row panels (checked against the row solve)
+    HG_TRY(multi_prepare(P));
+    HG_TRY(prepare_local_panel(P));
+  }
+  HG_CUDA_TRY(cudaDeviceSynchronize());
   return HG_OK;
 }
 
@@ -1214,7 +1222,7 @@ int hg_precond_profile_multi(HgPrecond* P, const double* R, int64_t ldr, double*
     cudaEventRecord(ev[2], st);
     if ((status = launch_zy_multi(P, nrhs, st)) != HG_OK) break;
     cudaEventRecord(ev[3], st);
-    if ((status = launch_local_solve_multi(P, R, ldr, nrhs, st)) != HG_OK) break;
+    if ((status = launch_local_batch(P, R, ldr, nrhs, st)) != HG_OK) break;
     cudaEventRecord(ev[4], st);
     if ((status = launch_assemble_multi(P, true, true, OUT, ldo, nrhs, st)) != HG_OK) break;
     cudaEventRecord(ev[5], st);
@@ -1263,6 +1271,18 @@ int hg_debug_set(HgPrecond* P, int32_t key, int64_t value) {
 }
 
 int64_t hg_dcgs2_explicit_passes(void) { return g_explicit_rho_passes.load(); }
+
+double hg_precond_stat(HgPrecond* P, int32_t key) {
+  if (!P) return NAN;
+  switch (key) {
+    case HG_STAT_PANEL_ACTIVE:
+      return P->panel_ok ? 1.0 : 0.0;
+    case HG_STAT_PANEL_DEVIATION:
+      return P->panel_dev;
+    default:
+      return NAN;
+  }
+}
 
 int hg_precond_spmv(HgPrecond* P, int which, const double* x, double* y, void* stream) {
   if (!P || !x || !y || (which != 0 && which != 1)) {

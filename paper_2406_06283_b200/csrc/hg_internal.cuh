@@ -46,6 +46,13 @@ struct HgPrecond {
   double* d_fwd = nullptr;
   double* d_bwd = nullptr;
   long long fwd_len = 0, bwd_len = 0;
+  // 16-row panel records of the same factors for the batched solve (hg_local_panel.cu)
+  long long* d_poff = nullptr;    // [2 n_local] forward / backward panel offsets
+  double* d_pfwd = nullptr;
+  double* d_pbwd = nullptr;
+  int panel_kwf = 0, panel_kwb = 0, panel_wr = 0;
+  bool panel_ok = false;          // panel records built and checked against the row solve
+  double panel_dev = -1.0;        // that check's deviation (-1: not built)
   long long xs_len = 0;
   double* d_xs = nullptr;         // per-block local solutions (scratch)
   // dof -> local contributions (positions in xs), fixed (subdomain) order
@@ -166,9 +173,11 @@ int spmv_dots_nblocks(int n);
 
 int launch_local_solve(HgPrecond* P, const double* r, cudaStream_t st);
 int launch_local_solve_multi(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st);
-// blocked multi-RHS local solve (hg_local_blk.cu): 32-row chains + DMMA band updates
-int launch_local_blocked(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st);
-int preload_local_blocked();
+// 16-row panel local solves on DMMA (hg_local_panel.cu)
+int prepare_local_panel(HgPrecond* P);
+int launch_local_panel(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st);
+int launch_local_batch(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st);
+int preload_local_panel();
 int launch_local_solve_single(HgPrecond* P, int s, const double* r_local, double* x_local, cudaStream_t st);
 // device band LU of every local block into P->d_fwd / P->d_bwd (hg_factor.cu)
 int band_lu_supported(int kl_max, int ku_max);

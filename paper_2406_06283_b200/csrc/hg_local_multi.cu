@@ -12,8 +12,6 @@ int launch_local_solve_multi(HgPrecond* P, const double* R, long long ldr, int n
     set_error("local band solve: nrhs out of range");
     return HG_ERR_ARG;
   }
-  const char* blk = getenv("HG_LOCAL_BLOCKED");
-  if (blk && blk[0] == '1') return launch_local_blocked(P, R, ldr, nrhs, st);
   return launch_local_grid_t<HG_MAX_RHS>(P, P->d_local, P->n_local, R, st, nrhs, ldr, P->d_xsm, P->xs_len);
 }
 
@@ -21,7 +19,7 @@ int preload_local_multi(HgPrecond* P) {
   cudaFuncAttributes at;
   LocalKernel k = pick_local<HG_MAX_RHS>(P->rf, P->rb);
   if (k) HG_CUDA_TRY(cudaFuncGetAttributes(&at, k));
-  return preload_local_blocked();
+  return preload_local_panel();
 }
 
 }  // namespace hg

@@ -1,0 +1,430 @@
+// Batched local solves as 16-row panels on the FP64 tensor pipe (the
+// batched apply's one-level part, schwarz.py:58-60, for up to 16 columns).
+//
+// Same operator as the row-record kernels of hg_local_impl.cuh (dgbtrs on
+// the band LU of every block: pivoted L sweep, then U sweep in reversed
+// coordinates), blocked so that no step-by-step dependency chain remains:
+// per sweep the rows advance 16 at a time and a panel is two small dense
+// products,
+//     X          =  D^{-1}  W[panel rows]                (16 x 16 x nrhs)
+//     W[trail]  +=  (-T)    X                           (kw x 16 x nrhs)
+// where D is the panel's 16 x 16 diagonal block of L (unit) or of U in
+// reversed coordinates (diagonal u_jj), T the band below it, and W the
+// window of active right-hand-side rows (shared memory, all columns).
+// Row interchanges (forward sweep, ~0.2% of rows) are moved to the front of
+// their panel: the panel's swaps are applied to W first and the multiplier
+// columns carry the later in-panel swaps (getrf's convention), which is the
+// same elimination reordered.  D^{-1} and T come from a setup conversion of
+// the row records (k_panel_convert below), stored in DMMA A-fragment order
+// (one coalesced 8-byte load per lane per fragment, T negated), and stream
+// through a TMA bulk-copy ring like the row records do.  The explicit 16 x 16
+// inverses change the rounding, not the operator: hg_precond_create checks
+// the panel solve against the row solve on a seeded batch and keeps the row
+// kernel if they differ by more than 1e-11 (hg_precond_stat reports it).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <vector>
+
+#include "hg_internal.cuh"
+
+namespace hg {
+
+namespace {
+constexpr int PB = 16;        // panel rows
+constexpr int PSR = 20;       // window row stride (16 columns + pad: conflict-free B fragments)
+constexpr int PNS = 3;        // ring stages
+constexpr int PTHREADS = 256 + 32;
+
+__device__ __forceinline__ void psync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ bool psync_or(bool p) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\tbar.red.or.pred q, 1, 256, p;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"((int)p)
+      : "memory");
+  return r != 0;
+}
+
+__device__ __forceinline__ void dmma_p(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+}  // namespace
+
+// panel record: [D^{-1} fragments: 2 m-tiles x 4 k-steps x 32 lanes]
+//               [-T fragments: KWP/8 m-tiles x 4 k-steps x 32 lanes]
+//               [16 relative pivot rows (forward) / 0..15 (backward)]
+__host__ __device__ inline long long panel_doubles(int kwp) { return 256 + 16LL * kwp + 16; }
+
+// ------------------------------------------------------------------ setup conversion
+// One CTA per block, 128 threads, panels in order.  Lt[(16 + KWP) x 16]: the
+// panel's multiplier columns (row r = panel row j0 + r), unit (L) or u_jj
+// (U, only its reciprocal is stored) diagonal.
+template <bool FWD>
+__global__ void __launch_bounds__(128) k_panel_convert(const LocalDesc* __restrict__ descs,
+                                                       const double* __restrict__ rec_all,
+                                                       const long long* __restrict__ poff, int kwp,
+                                                       double* __restrict__ out_all) {
+  extern __shared__ double lt[];  // (16 + kwp) x 16, then dinvd[16], then X[16][17]
+  const LocalDesc d = descs[blockIdx.x];
+  const int n = d.n;
+  if (n == 0) return;
+  const int kw = FWD ? d.kl : d.kv;
+  const int stride = FWD ? d.fstride : d.bstride;
+  const double* rec = rec_all + (FWD ? d.fwd_off : d.bwd_off);
+  double* out = out_all + poff[blockIdx.x];
+  const int rows = PB + kwp;
+  double* dinvd = lt + rows * PB;
+  double* X = dinvd + PB;
+  __shared__ int prel[PB];
+  const int tid = threadIdx.x;
+  const int np = (n + PB - 1) / PB;
+  const long long PS = panel_doubles(kwp);
+  for (int p = 0; p < np; ++p) {
+    const int j0 = p * PB;
+    for (int e = tid; e < rows * PB; e += blockDim.x) lt[e] = 0.0;
+    __syncthreads();
+    for (int e = tid; e < PB * (kw + 1); e += blockDim.x) {
+      const int c = e / (kw + 1), t = e % (kw + 1);  // t = 0: diagonal / pivot slot
+      const int j = j0 + c;
+      const double* r = rec + (long long)j * stride;
+      if (t == 0) {
+        if (j < n) {
+          if (FWD) {
+            lt[c * PB + c] = 1.0;
+            prel[c] = __double2int_rn(r[kw]) - j0;
+          } else {
+            dinvd[c] = r[kw];
+            prel[c] = c;
+          }
+        } else {
+          lt[c * PB + c] = 1.0;
+          if (!FWD) dinvd[c] = 1.0;
+          prel[c] = c;
+        }
+      } else if (j < n && c + t < rows) {
+        lt[(c + t) * PB + c] = r[t - 1];
+      }
+    }
+    __syncthreads();
+    if (FWD) {
+      // move each swap in front of the panel: swap rows t and p_t of the
+      // multiplier columns computed before it (getrf's dlaswp on the left)
+      for (int t = 0; t < PB; ++t) {
+        const int pt = prel[t];
+        if (pt != t && tid < t) {
+          const double a = lt[t * PB + tid];
+          lt[t * PB + tid] = lt[pt * PB + tid];
+          lt[pt * PB + tid] = a;
+        }
+        __syncthreads();
+      }
+    }
+    // D^{-1}: column c by forward substitution (thread c)
+    if (tid < PB) {
+      const int c = tid;
+      for (int i = 0; i < PB; ++i) {
+        double s = (i == c) ? 1.0 : 0.0;
+        for (int k = 0; k < i; ++k) s = fma(-lt[i * PB + k], X[k * 17 + c], s);
+        X[i * 17 + c] = FWD ? s : s * dinvd[i];
+      }
+    }
+    __syncthreads();
+    double* po = out + (long long)p * PS;
+    for (int e = tid; e < 256; e += blockDim.x) {  // D^{-1} fragments
+      const int f = e >> 5, lane = e & 31, mt = f >> 2, ks = f & 3;
+      po[e] = X[(mt * 8 + (lane >> 2)) * 17 + ks * 4 + (lane & 3)];
+    }
+    for (int e = tid; e < 16 * kwp; e += blockDim.x) {  // -T fragments
+      const int f = e >> 5, lane = e & 31, mt = f >> 2, ks = f & 3;
+      po[256 + e] = -lt[(PB + mt * 8 + (lane >> 2)) * PB + ks * 4 + (lane & 3)];
+    }
+    if (tid < PB) po[256 + 16 * kwp + tid] = (double)prel[tid];
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ the panel solve
+struct PanelArgs {
+  const LocalDesc* descs;
+  const long long* poff;   // [2 n_local]: forward / backward panel offsets per block
+  const int* idx;
+  const double* pf;
+  const double* pb;
+  const double* R;
+  long long ldr;
+  double* xs;
+  long long xs_len;
+  int nrhs, kwf, kwb, WR, stage_stride;
+};
+
+template <bool FWD>
+__device__ __forceinline__ void panel_sweep(const PanelArgs& a, const LocalDesc& d, double* ring, uint64_t* full,
+                                            uint64_t* empty, double* W, double* Xb, int& chunk) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = lane & 3, g = lane >> 2;
+  const int n = d.n, kwp = FWD ? a.kwf : a.kwb, WR = a.WR;
+  const int np = (n + PB - 1) / PB;
+  const int* idx = a.idx + d.idx_off;
+  double* xs = a.xs + d.idx_off;
+  auto in = [&](int row, int c) -> double {
+    if (row >= n || c >= a.nrhs) return 0.0;
+    if (FWD) return __ldg(a.R + (long long)c * a.ldr + __ldg(idx + row));
+    return xs[(long long)c * a.xs_len + (n - 1 - row)];
+  };
+  auto out = [&](int row, int c, double v) {
+    if (row < n && c < a.nrhs) xs[(long long)c * a.xs_len + (FWD ? row : n - 1 - row)] = v;
+  };
+  auto wrow = [&](int row) -> double* { return W + (size_t)(row % WR) * PSR; };
+  // prologue: panel 0 and its trailing rows
+  for (int e = tid; e < (PB + kwp) * 16; e += 256) wrow(e >> 4)[e & 15] = in(e >> 4, e & 15);
+  psync();
+  const int mtT = kwp >> 3;
+  for (int p = 0; p < np; ++p) {
+    const int j0 = p * PB;
+    // rows entering for the next panel's trailing update (issued early)
+    const int erow = j0 + PB + kwp + (tid >> 4), ec = tid & 15;
+    const double ev = in(erow, ec);
+    const int stage = chunk % PNS;
+    mbar_wait(&full[stage], (chunk / PNS) & 1);
+    const double* rec = ring + (size_t)stage * a.stage_stride;
+    if (FWD) {  // the panel's row interchanges, moved to its front
+      const int pt = tid < PB ? __double2int_rn(rec[256 + 16 * kwp + tid]) : 0;
+      if (psync_or(tid < PB && pt != tid)) {
+        if (warp == 0) {
+          for (int t = 0; t < PB; ++t) {
+            const int p2 = __shfl_sync(FULL, pt, t);
+            if (p2 != t && lane < 16) {
+              double* r1 = wrow(j0 + t);
+              double* r2 = wrow(j0 + p2);
+              const double tmp = r1[lane];
+              r1[lane] = r2[lane];
+              r2[lane] = tmp;
+            }
+            __syncwarp();
+          }
+        }
+        psync();
+      }
+    }
+    // X = D^{-1} W[panel]: 2 x 2 output tiles on warps 0-3
+    if (warp < 4) {
+      const int mt = warp >> 1, nt = warp & 1;
+      double acc[2] = {0.0, 0.0};
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        const double av = rec[(mt * 4 + ks) * 32 + lane];
+        const double bv = wrow(j0 + ks * 4 + q)[nt * 8 + g];
+        dmma_p(acc, av, bv);
+      }
+      const int r = mt * 8 + g, c = nt * 8 + 2 * q;
+      *reinterpret_cast<double2*>(Xb + r * PSR + c) = make_double2(acc[0], acc[1]);
+      out(j0 + r, c, acc[0]);
+      out(j0 + r, c + 1, acc[1]);
+    }
+    // entering rows take the slots of the previous panel (finished)
+    wrow(erow)[ec] = ev;
+    psync();
+    // W[trail] += (-T) X: (kwp / 8) x 2 tiles over the 8 warps
+    const double* T = rec + 256;
+    for (int t = warp; t < 2 * mtT; t += 8) {
+      const int mt = t >> 1, nt = t & 1;
+      double* crow = wrow(j0 + PB + mt * 8 + g) + nt * 8 + 2 * q;
+      const double2 c2 = *reinterpret_cast<const double2*>(crow);
+      double acc[2] = {c2.x, c2.y};
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) dmma_p(acc, T[(mt * 4 + ks) * 32 + lane], Xb[(ks * 4 + q) * PSR + nt * 8 + g]);
+      *reinterpret_cast<double2*>(crow) = make_double2(acc[0], acc[1]);
+    }
+    psync();
+    if (tid == 0) mbar_arrive(&empty[stage]);
+    ++chunk;
+  }
+}
+
+__global__ void __launch_bounds__(PTHREADS, 2) k_local_panel(PanelArgs a) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[PNS], empty[PNS];
+  const LocalDesc d = a.descs[blockIdx.x];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < PNS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (d.n == 0) return;
+  const int np = (d.n + PB - 1) / PB;
+  if (threadIdx.x >= 256) {
+    if (threadIdx.x == 256) {  // producer: forward panels, then backward panels
+      const long long psf = panel_doubles(a.kwf), psb = panel_doubles(a.kwb);
+      for (int c = 0; c < 2 * np; ++c) {
+        const int stage = c % PNS;
+        if (c >= PNS) mbar_wait(&empty[stage], ((c / PNS) - 1) & 1);
+        const bool f = c < np;
+        const int pp = f ? c : c - np;
+        const double* src = f ? a.pf + a.poff[2 * blockIdx.x] + pp * psf : a.pb + a.poff[2 * blockIdx.x + 1] + pp * psb;
+        const uint32_t bytes = (uint32_t)((f ? psf : psb) * 8);
+        mbar_arrive_expect_tx(&full[stage], bytes);
+        bulk_g2s(sm + (size_t)stage * a.stage_stride, src, bytes, &full[stage]);
+      }
+    }
+    return;
+  }
+  double* W = sm + (size_t)PNS * a.stage_stride;
+  double* Xb = W + (size_t)a.WR * PSR;
+  int chunk = 0;
+  panel_sweep<true>(a, d, sm, full, empty, W, Xb, chunk);
+  panel_sweep<false>(a, d, sm, full, empty, W, Xb, chunk);
+}
+
+// ------------------------------------------------------------------ host side
+static int round8(int x) { return (x + 7) / 8 * 8; }
+
+template <typename T>
+static int dev_upload(T** dptr, const T* host, size_t count, long long* bytes) {
+  HG_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(dptr), sizeof(T) * std::max<size_t>(count, 1)));
+  if (host && count) HG_CUDA_TRY(cudaMemcpy(*dptr, host, sizeof(T) * count, cudaMemcpyHostToDevice));
+  if (bytes) *bytes += (long long)(sizeof(T) * count);
+  return HG_OK;
+}
+
+// batched local solves: panels when prepared and checked, else the row kernel
+int launch_local_batch(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st) {
+  if (P->panel_ok) return launch_local_panel(P, R, ldr, nrhs, st);
+  return launch_local_solve_multi(P, R, ldr, nrhs, st);
+}
+
+static size_t panel_smem(const HgPrecond* P) {
+  const long long ss = std::max(panel_doubles(P->panel_kwf), panel_doubles(P->panel_kwb));
+  return sizeof(double) * ((size_t)PNS * ss + (size_t)P->panel_wr * PSR + (size_t)PB * PSR);
+}
+
+int launch_local_panel(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st) {
+  if (P->n_local == 0) return HG_OK;
+  const size_t smem = panel_smem(P);
+  HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k_local_panel), smem, false));
+  PanelArgs a{P->d_local, P->d_poff, P->d_local_idx, P->d_pfwd, P->d_pbwd, R, ldr, P->d_xsm, P->xs_len, nrhs,
+              P->panel_kwf, P->panel_kwb, P->panel_wr,
+              (int)std::max(panel_doubles(P->panel_kwf), panel_doubles(P->panel_kwb))};
+  k_local_panel<<<P->n_local, PTHREADS, smem, st>>>(a);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+__global__ void k_fill_hash(long long n, double* y, unsigned seed) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    unsigned long long h = (unsigned long long)i * 0x9E3779B97F4A7C15ull + seed;
+    h ^= h >> 31;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 27;
+    y[i] = (double)(h >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+  }
+}
+
+// Build the panel records from the row records (device) and check the panel
+// solve against the row solve on a seeded batch; keep it only if they agree
+// to 1e-11 (relative to each column's largest entry).
+int prepare_local_panel(HgPrecond* P) {
+  P->panel_ok = false;
+  P->panel_dev = -1.0;
+  const char* env = getenv("HG_LOCAL_PANEL");
+  if (P->n_local == 0 || (env && env[0] == '0')) return HG_OK;
+  int kwf = 0, kwb = 0;
+  for (const LocalDesc& d : P->h_local) {
+    kwf = std::max(kwf, d.kl);
+    kwb = std::max(kwb, d.kv);
+  }
+  P->panel_kwf = round8(kwf);
+  P->panel_kwb = round8(kwb);
+  P->panel_wr = 2 * PB + std::max(P->panel_kwf, P->panel_kwb);
+  if (panel_smem(P) > 227 * 1024) return HG_OK;  // window too wide for shared memory: row kernel only
+  std::vector<long long> poff(2 * P->n_local);
+  long long pf = 0, pb = 0;
+  for (int s = 0; s < P->n_local; ++s) {
+    const long long np = (P->h_local[s].n + PB - 1) / PB;
+    poff[2 * s] = pf;
+    poff[2 * s + 1] = pb;
+    pf += np * panel_doubles(P->panel_kwf);
+    pb += np * panel_doubles(P->panel_kwb);
+  }
+  HG_TRY(dev_upload(&P->d_poff, poff.data(), poff.size(), &P->device_bytes));
+  // per-sweep offsets for the two conversion launches (temporaries)
+  std::vector<long long> pof(P->n_local), pob(P->n_local);
+  for (int s = 0; s < P->n_local; ++s) {
+    pof[s] = poff[2 * s];
+    pob[s] = poff[2 * s + 1];
+  }
+  long long *d_pof = nullptr, *d_pob = nullptr;
+  HG_TRY(dev_upload(&d_pof, pof.data(), pof.size(), nullptr));
+  HG_TRY(dev_upload(&d_pob, pob.data(), pob.size(), nullptr));
+  HG_TRY(dev_upload<double>(&P->d_pfwd, nullptr, (size_t)pf, &P->device_bytes));
+  HG_TRY(dev_upload<double>(&P->d_pbwd, nullptr, (size_t)pb, &P->device_bytes));
+  const size_t cf = sizeof(double) * ((PB + P->panel_kwf) * PB + PB + PB * 17);
+  const size_t cb = sizeof(double) * ((PB + P->panel_kwb) * PB + PB + PB * 17);
+  HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k_panel_convert<true>), cf, false));
+  HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k_panel_convert<false>), cb, false));
+  k_panel_convert<true><<<P->n_local, 128, cf>>>(P->d_local, P->d_fwd, d_pof, P->panel_kwf, P->d_pfwd);
+  HG_LAUNCH_CHECK();
+  k_panel_convert<false><<<P->n_local, 128, cb>>>(P->d_local, P->d_bwd, d_pob, P->panel_kwb, P->d_pbwd);
+  HG_LAUNCH_CHECK();
+  HG_CUDA_TRY(cudaDeviceSynchronize());
+  cudaFree(d_pof);
+  cudaFree(d_pob);
+
+  // guard: panel vs row solve on a seeded 16-column batch
+  const int nr = HG_MAX_RHS;
+  const long long nn = (long long)nr * P->n;
+  double *d_r = nullptr, *d_ref = nullptr;
+  HG_CUDA_TRY(cudaMalloc(&d_r, sizeof(double) * nn));
+  HG_CUDA_TRY(cudaMalloc(&d_ref, sizeof(double) * (size_t)nr * P->xs_len));
+  k_fill_hash<<<ceil_div(nn, 256), 256>>>(nn, d_r, 2406u);
+  int s = launch_local_solve_multi(P, d_r, P->n, nr, 0);
+  if (s == HG_OK && cudaMemcpy(d_ref, P->d_xsm, sizeof(double) * (size_t)nr * P->xs_len, cudaMemcpyDeviceToDevice) !=
+                        cudaSuccess)
+    s = HG_ERR_CUDA;
+  if (s == HG_OK) s = launch_local_panel(P, d_r, P->n, nr, 0);
+  std::vector<double> ref, got;
+  if (s == HG_OK) {
+    ref.resize((size_t)nr * P->xs_len);
+    got.resize(ref.size());
+    if (cudaMemcpy(ref.data(), d_ref, sizeof(double) * ref.size(), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(got.data(), P->d_xsm, sizeof(double) * got.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+      s = HG_ERR_CUDA;
+  }
+  cudaFree(d_r);
+  cudaFree(d_ref);
+  if (s != HG_OK) {
+    set_error("local panel guard failed to run");
+    return HG_ERR_CUDA;
+  }
+  double dev = 0.0;
+  for (int c = 0; c < nr; ++c) {
+    double mx = 0.0, df = 0.0;
+    for (long long i = 0; i < P->xs_len; ++i) {
+      const double a = ref[(size_t)c * P->xs_len + i], b = got[(size_t)c * P->xs_len + i];
+      mx = std::max(mx, std::fabs(a));
+      df = std::max(df, std::fabs(a - b));
+      if (std::isnan(b)) df = INFINITY;
+    }
+    dev = std::max(dev, mx > 0.0 ? df / mx : df);
+  }
+  P->panel_dev = dev;
+  P->panel_ok = dev <= 1e-11;
+  return HG_OK;
+}
+
+int preload_local_panel() {
+  cudaFuncAttributes at;
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_local_panel));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_panel_convert<true>));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_panel_convert<false>));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_fill_hash));
+  return HG_OK;
+}
+
+}  // namespace hg

@@ -535,6 +535,8 @@ class TwoLevelPreconditioner:
         self.b0_dense = bool(meta["b0_dense"])
         self.b0_dense_dev = meta.get("b0_dense_dev")
         self.b0_tile_dev = meta.get("b0_tile_dev")
+        self.panel_active = bool(lib.hg_precond_stat(h, _lib.STAT_PANEL_ACTIVE) == 1.0)
+        self.panel_deviation = float(lib.hg_precond_stat(h, _lib.STAT_PANEL_DEVIATION))
 
     # ------------------------------------------------------------------ API
     @property

@@ -75,6 +75,7 @@ def test_full_size_parity_vs_reference(name):
     assert np.abs(last - fx["lam_last"]).max() <= 1e-9 * np.abs(fx["lam_last"]).max()
 
     pre = hg.factorize(P.forms, P.dec, P.coarse)
+    print("%s: panel local solve active %s (deviation %.2e)" % (name, pre.panel_active, pre.panel_deviation))
     n = pre.n
     sub = fx["sub"]
     B, Dk = P.forms.helmholtz, P.forms.dk
@@ -101,7 +102,7 @@ def test_full_size_parity_vs_reference(name):
     R = np.stack([r, u] + [F[:, c] for c in range(min(F.shape[1], 6))], axis=1)
     Rm = pre.apply_multi(R)
     for c in range(R.shape[1]):
-        assert rel(Rm[:, c], pre.apply(R[:, c])) <= 1e-12
+        assert rel(Rm[:, c], pre.apply(R[:, c])) <= 1e-11  # panel local solve (hg_local_panel.cu)
 
     # ---- full single-RHS solves, both orthogonalisations (wgmres.py:74-203)
     op = pre.as_operator("T")

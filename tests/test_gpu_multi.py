@@ -3,7 +3,7 @@
 batch: every column is checked against the one-at-a-time device path (itself
 pinned to the reference's golden vectors in test_gpu_parity.py) and, where
 cheap, against the CPU oracle / the reference's golden values directly.
-Bars: apply columns rel <= 1e-12 vs the single apply (1e-10 vs the reference),
+Bars: apply columns rel <= 1e-11 vs the single apply (1e-10 vs the reference),
 SpMM bitwise, GMRES iterations +-1 and solution rel <= 1e-8 per column."""
 
 import os
@@ -21,6 +21,9 @@ pytestmark = pytest.mark.gpu
 
 APPLY_RTOL = 1e-10
 SOL_RTOL = 1e-8
+# a batched column vs the single apply: the batched local solve runs on 16-row
+# panels with explicit 16 x 16 inverses (hg_local_panel.cu), checked at 1e-11
+MULTI_RTOL = 1e-11
 
 
 def rel(a, b):
@@ -60,12 +63,12 @@ def test_apply_multi_matches_single(cfg1, nrhs):
     R[:, 0] = g["r"]
     got = pre.apply_multi(R)
     want = np.stack([pre.apply(R[:, c]) for c in range(nrhs)], axis=1)
-    assert colrel(got, want) <= 1e-12
+    assert colrel(got, want) <= MULTI_RTOL
     assert rel(got[:, 0], g["apply_r"]) <= APPLY_RTOL  # the reference's own value
     # deterministic, and the batched operator T = M^-1 B too
     assert np.array_equal(pre.apply_multi(R), got)
     T = pre.as_operator("T").apply_multi(R)
-    assert colrel(T, np.stack([pre.apply_T(R[:, c]) for c in range(nrhs)], axis=1)) <= 1e-12
+    assert colrel(T, np.stack([pre.apply_T(R[:, c]) for c in range(nrhs)], axis=1)) <= MULTI_RTOL
 
 
 def test_apply_multi_zero_columns_and_device_tensors(cfg1):
@@ -93,10 +96,10 @@ def test_apply_multi_one_level(cfg1):
     got = pre1.apply_multi(R)
     assert rel(got[:, 1], g["apply_one_level_r"]) <= APPLY_RTOL
     want = np.stack([pre1.apply(R[:, c]) for c in range(5)], axis=1)
-    if os.environ.get("HG_LOCAL_BLOCKED", "0") == "1":  # blocked solve: DMMA band updates, different rounding
-        assert colrel(got, want) <= 1e-12
+    if pre1.panel_active:  # 16-row panel solve: explicit 16 x 16 inverses, different rounding
+        assert colrel(got, want) <= MULTI_RTOL
     else:
-        assert np.array_equal(got, want)  # no coarse part: same per-column arithmetic, bitwise
+        assert np.array_equal(got, want)  # row kernel, no coarse part: same per-column arithmetic, bitwise
 
 
 def test_apply_multi_unpremultiplied_coarse_tiles(cfg1, monkeypatch):
@@ -110,7 +113,7 @@ def test_apply_multi_unpremultiplied_coarse_tiles(cfg1, monkeypatch):
     R[:, 5] = g["r"]
     got = pre0.apply_multi(R)
     want = np.stack([pre0.apply(R[:, c]) for c in range(16)], axis=1)
-    assert colrel(got, want) <= 1e-12
+    assert colrel(got, want) <= MULTI_RTOL
     assert rel(got[:, 5], g["apply_r"]) <= APPLY_RTOL
 
 
@@ -189,7 +192,7 @@ def test_config_batch_parity_vs_oracle(name):
     for c in (0, 7, 15):
         assert rel(got[:, c], orc.apply(R[:, c])) <= APPLY_RTOL
     want = np.stack([pre.apply(R[:, c]) for c in range(16)], axis=1)
-    assert colrel(got, want) <= 1e-12
+    assert colrel(got, want) <= MULTI_RTOL
     B, Dk = P.forms.helmholtz, P.forms.dk
     F = np.stack([P.rhs, R[:, 1]], axis=1)
     X, reps = hg.weighted_gmres_batch(pre.as_operator("T"), pre.apply_multi(F), weight=Dk, rtol=1e-6, maxit=1000)
@@ -218,7 +221,7 @@ def test_coarse_solve_modes_agree(name, monkeypatch):
         for k, c in enumerate((0, 9)):
             assert rel(single[:, k], orc.apply_coarse(R[:, c])) <= APPLY_RTOL
         assert rel(outs[dense][0], orc.apply(R[:, 0])) <= APPLY_RTOL
-        assert colrel(outs[dense][1], np.stack([pre.apply(R[:, c]) for c in range(16)], axis=1)) <= 1e-12
+        assert colrel(outs[dense][1], np.stack([pre.apply(R[:, c]) for c in range(16)], axis=1)) <= MULTI_RTOL
     assert rel(outs["1"][0], outs["0"][0]) <= 1e-12
     assert colrel(outs["1"][1], outs["0"][1]) <= 1e-12
 
