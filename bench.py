@@ -178,13 +178,16 @@ def multi_stage_bytes(pre, nr):
     """Algorithmic bytes of one batched apply of nr columns (factors, Z and
     B0 streamed once; vector traffic per column)."""
     nloc = pre.local_sizes
-    loc = sum(8 * n * (kl + kv + 1) + 4 * n + 4 * n for n, (kl, kv) in zip(nloc, pre.local_bands))
+    if getattr(pre, "panel_bytes", None):  # 16-row panel records (hg_local_panel.cu) + idx
+        loc = pre.panel_bytes + sum(4 * n for n in nloc)
+    else:
+        loc = sum(8 * n * (kl + kv + 1) + 4 * n + 4 * n for n, (kl, kv) in zip(nloc, pre.local_bands))
     loc += nr * sum(16 * n for n in nloc)  # gather r + write x_s per column
     zt = zy = b0 = 0
     if pre.has_coarse:
         zt = sum(8 * n * m + 4 * n + 8 * n * nr for n, m in pre.cblock_shapes)
         zy = sum(8 * n * m + 8 * n * nr for n, m in pre.cblock_shapes) + 8 * pre.m * nr
-        b0 = pre.b0_bytes
+        b0 = pre.b0_bytes_multi
     asm = nr * (8 * sum(nloc) + (8 * sum(n for n, _ in pre.cblock_shapes) if pre.has_coarse else 0) + 8 * pre.n)
     return {"zt": zt, "b0_solve": b0, "zy": zy, "local": loc, "assemble": asm}
 

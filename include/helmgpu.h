@@ -177,6 +177,9 @@ typedef struct {
   int64_t lcsr_nnz;
   int32_t* factor_info;
   double* factor_min_pivot;
+  /* With b0_inv given: 0 = every apply uses it; 1 = only batched applies
+   * (the single-RHS apply keeps the panel chain, which is shorter there). */
+  int32_t b0_inv_batched_only;
 } HgPrecondDesc;
 
 /* ---- library ---- */

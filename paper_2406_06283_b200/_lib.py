@@ -70,6 +70,7 @@ class HgPrecondDesc(ctypes.Structure):
         ("lcsr_nnz", ctypes.c_int64),
         ("factor_info", _i32p),
         ("factor_min_pivot", _f64p),
+        ("b0_inv_batched_only", ctypes.c_int32),
     ]
 
 

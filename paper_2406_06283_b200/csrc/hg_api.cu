@@ -522,7 +522,7 @@ static int precond_apply_core(HgPrecond* P, const double* r, double* out, const 
 
 static int precond_apply_core_impl(HgPrecond* P, const double* r, double* out, const double* W, long long ldw,
                                    int nv, double* partials, int* nb, cudaStream_t st) {
-  if (P->m > 0 && P->d_b0_inv) {
+  if (P->m > 0 && P->d_b0_inv && P->b0_inv_single) {
     // dense coarse mode: Z^T r, then (side stream) c -> B0^{-1} c -> Z y beside the local solves
     HG_TRY(launch_zt(P, r, st));
     HG_CUDA_TRY(cudaEventRecord(P->ev_fork, st));
@@ -557,7 +557,7 @@ static int precond_apply_core_impl(HgPrecond* P, const double* r, double* out, c
 
 // coarse solve of the current Z^T r partials on one stream (apply_coarse, profiling)
 static int coarse_solve_serial(HgPrecond* P, cudaStream_t st) {
-  if (P->d_b0_inv) return launch_b0_dense(P, st);
+  if (P->d_b0_inv && P->b0_inv_single) return launch_b0_dense(P, st);
   return launch_coarse_solve(P, st);
 }
 
@@ -1043,6 +1043,7 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
     HG_TRY(upload<double>(&P->d_y, nullptr, (size_t)P->m, bytes));
     if (D->b0_inv) {
       HG_TRY(upload(&P->d_b0_inv, D->b0_inv, (size_t)P->m * P->m, bytes));
+      P->b0_inv_single = D->b0_inv_batched_only == 0;
       HG_TRY(upload<double>(&P->d_c, nullptr, (size_t)P->m, bytes));
     }
     HG_TRY(upload<double>(&P->d_zs, nullptr, (size_t)std::max(nidx, 1LL), bytes));

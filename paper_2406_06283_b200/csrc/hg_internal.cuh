@@ -97,6 +97,7 @@ struct HgPrecond {
   int skip_zt = 0;                // fault injection (hg_debug_set): Z^T r launches to drop
   double* d_y = nullptr;          // coarse solution (m)
   double* d_b0_inv = nullptr;     // dense B0^{-1} (m x m row-major) or null
+  bool b0_inv_single = true;      // single-RHS applies use it too (else only the batched ones)
   double* d_c = nullptr;          // reduced Z^T r (m), dense mode
   double* d_cm = nullptr;         // [m][16] reduced Z^T R, dense mode
   double* d_ypart = nullptr;      // [B0_KSPLIT][m][16] split-K partials, dense batched mode

@@ -33,7 +33,8 @@ namespace hg {
 namespace {
 constexpr int PB = 16;        // panel rows
 constexpr int PSR = 20;       // window row stride (16 columns + pad: conflict-free B fragments)
-constexpr int PNS = 3;        // ring stages
+constexpr int PNS = 4;        // ring stages
+constexpr int PD = 4;         // panels of look-ahead for the entering rows (a gather is two dependent loads)
 constexpr int PTHREADS = 256 + 32;
 
 __device__ __forceinline__ void psync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
@@ -180,13 +181,22 @@ __device__ __forceinline__ void panel_sweep(const PanelArgs& a, const LocalDesc&
   auto wrow = [&](int row) -> double* { return W + (size_t)(row % WR) * PSR; };
   // prologue: panel 0 and its trailing rows
   for (int e = tid; e < (PB + kwp) * 16; e += 256) wrow(e >> 4)[e & 15] = in(e >> 4, e & 15);
+  // rows entering at panels 0..PD-1, in flight ahead of their use (this
+  // thread's row tid / 16, column tid % 16 of each 16-row group)
+  const int er = tid >> 4, ec = tid & 15;
+  double ev[PD];
+#pragma unroll
+  for (int k = 0; k < PD; ++k) ev[k] = in(PB + kwp + PB * k + er, ec);
   psync();
   const int mtT = kwp >> 3;
   for (int p = 0; p < np; ++p) {
     const int j0 = p * PB;
-    // rows entering for the next panel's trailing update (issued early)
-    const int erow = j0 + PB + kwp + (tid >> 4), ec = tid & 15;
-    const double ev = in(erow, ec);
+    // rows entering for the next panel's trailing update (loaded PD panels ago)
+    const int erow = j0 + PB + kwp + er;
+    const double evc = ev[0];
+#pragma unroll
+    for (int k = 0; k + 1 < PD; ++k) ev[k] = ev[k + 1];
+    ev[PD - 1] = in(erow + PB * PD, ec);
     const int stage = chunk % PNS;
     mbar_wait(&full[stage], (chunk / PNS) & 1);
     const double* rec = ring + (size_t)stage * a.stage_stride;
@@ -225,7 +235,7 @@ __device__ __forceinline__ void panel_sweep(const PanelArgs& a, const LocalDesc&
       out(j0 + r, c + 1, acc[1]);
     }
     // entering rows take the slots of the previous panel (finished)
-    wrow(erow)[ec] = ev;
+    wrow(erow)[ec] = evc;
     psync();
     // W[trail] += (-T) X: (kwp / 8) x 2 tiles over the 8 warps
     const double* T = rec + 256;

@@ -466,8 +466,9 @@ class TwoLevelPreconditioner:
             # dense mode: B0^{-1} applied as a streaming GEMV / DMMA GEMM beside the
             # local solves; kept only if it agrees with getrs (the reference's lu_solve)
             M["b0_dense_dev"] = None
-            dense = os.environ.get("HG_B0_DENSE", "0")  # measured slower by default: see DESIGN.md section 8
-            if dense == "1" or (dense == "auto" and m <= 20000):  # "auto": whenever it fits
+            # "1": every apply; "multi": batched applies only (the single apply keeps the chain)
+            dense = os.environ.get("HG_B0_DENSE", "0")
+            if dense in ("1", "multi") or (dense == "auto" and m <= 20000):  # "auto": whenever it fits
                 torch = _torch()
                 B0 = np.ascontiguousarray(np.asarray(self._coarse.B0), dtype=np.float64)
                 Binv = torch.linalg.inv(torch.from_numpy(B0).cuda())
@@ -481,8 +482,11 @@ class TwoLevelPreconditioner:
                 M["b0_dense_dev"] = ddev
                 if ddev <= 1e-11:
                     M["b0_dense"] = True
+                    M["b0_inv_batched_only"] = 1 if dense == "multi" else 0
                     put("b0_inv", Binv, f64)
-                    M["b0_bytes"] = int(8 * m * m + 16 * m)
+                    M["b0_bytes_multi"] = int(8 * m * m + 16 * m)
+                    if dense != "multi":
+                        M["b0_bytes"] = int(8 * m * m + 16 * m)
             M["n_cblk"] = len(cblocks)
             put("cblk_n", [i.size for i, _ in cblocks], i32)
             put("cblk_m", [b.shape[1] for _, b in cblocks], i32)
@@ -531,12 +535,21 @@ class TwoLevelPreconditioner:
         self.local_bands = [tuple(b) for b in meta["local_bands"]]
         self.cblock_shapes = [tuple(c) for c in meta["cblock_shapes"]]
         self.b0_bytes = int(meta["b0_bytes"])
+        self.b0_bytes_multi = int(meta.get("b0_bytes_multi", meta["b0_bytes"]))
         self.b0_mode = int(meta["b0_mode"])
         self.b0_dense = bool(meta["b0_dense"])
         self.b0_dense_dev = meta.get("b0_dense_dev")
         self.b0_tile_dev = meta.get("b0_tile_dev")
         self.panel_active = bool(lib.hg_precond_stat(h, _lib.STAT_PANEL_ACTIVE) == 1.0)
         self.panel_deviation = float(lib.hg_precond_stat(h, _lib.STAT_PANEL_DEVIATION))
+        # factor bytes one batched local solve streams (16-row panel records, hg_local_panel.cu)
+        if self.panel_active and "local_kl" in arrays and len(arrays["local_kl"]):
+            r8 = lambda x: (int(x) + 7) // 8 * 8  # noqa: E731
+            kwf, kwb = r8(np.max(arrays["local_kl"])), r8(np.max(arrays["local_kv"]))
+            npan = sum((int(x) + 15) // 16 for x in arrays["local_n"])
+            self.panel_bytes = 8 * npan * ((256 + 16 * kwf + 16) + (256 + 16 * kwb + 16))
+        else:
+            self.panel_bytes = None
 
     # ------------------------------------------------------------------ API
     @property
