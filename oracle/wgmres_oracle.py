@@ -12,7 +12,11 @@ import numpy as np
 import scipy.linalg
 
 
-def weighted_gmres(op, rhs, weight=None, rtol=1e-6, maxit=200, x0=None):
+def weighted_gmres(op, rhs, weight=None, rtol=1e-6, maxit=200, x0=None, basis_state=None):
+    """``basis_state`` (timing slices of the CPU baseline only): (V, WV), a
+    list of j+1 basis vectors and their W images to resume from, so that
+    iterations j, j+1, ... run with the cost they have deep into a solve (the
+    per-iteration work grows with j); the returned x is then meaningless."""
     apply = op if callable(op) else (lambda v: op @ v)
     rhs = np.asarray(rhs, dtype=float)
     n = rhs.size
@@ -23,16 +27,22 @@ def weighted_gmres(op, rhs, weight=None, rtol=1e-6, maxit=200, x0=None):
     beta = float(np.sqrt(r0 @ wr0))
     if beta == 0.0:
         return x0.copy(), dict(iterations=0, history=np.array([0.0]), converged=True, breakdown=False, reorth=0)
-    maxit = int(min(maxit, n))
-    basis, wbasis = [r0 / beta], [wr0 / beta]
+    j_start = 0
+    if basis_state is not None:
+        basis, wbasis = list(basis_state[0]), list(basis_state[1])
+        j_start = len(basis) - 1
+        maxit = int(min(maxit + j_start, n))
+    else:
+        maxit = int(min(maxit, n))
+        basis, wbasis = [r0 / beta], [wr0 / beta]
     H = np.zeros((maxit + 1, maxit))
-    cs, sn = np.zeros(maxit), np.zeros(maxit)
+    cs, sn = np.ones(maxit), np.zeros(maxit)
     g = np.zeros(maxit + 1)
-    g[0] = beta
+    g[j_start] = beta
     hist = [beta]
     converged = breakdown = False
     reorth = 0
-    for j in range(maxit):
+    for j in range(j_start, maxit):
         w = np.array(apply(basis[j]), dtype=float, copy=True)
         col = np.zeros(j + 2)
         for i in range(j + 1):
@@ -69,6 +79,9 @@ def weighted_gmres(op, rhs, weight=None, rtol=1e-6, maxit=200, x0=None):
             converged = True
             break
     m = len(hist) - 1
+    if j_start:
+        return None, dict(iterations=m, history=np.asarray(hist), converged=converged, breakdown=breakdown,
+                          reorth=reorth)
     y = scipy.linalg.solve_triangular(H[:m, :m], g[:m], lower=False) if m else np.zeros(0)
     x = x0 + (np.column_stack(basis[:m]) @ y if m else 0.0)
     return x, dict(iterations=m, history=np.asarray(hist), converged=converged, breakdown=breakdown, reorth=reorth)

@@ -5,12 +5,14 @@
 // the band LU of every block: pivoted L sweep, then U sweep in reversed
 // coordinates), blocked so that no step-by-step dependency chain remains:
 // per sweep the rows advance 16 at a time and a panel is two small dense
-// products,
-//     X          =  D^{-1}  W[panel rows]                (16 x 16 x nrhs)
-//     W[trail]  +=  (-T)    X                           (kw x 16 x nrhs)
+// products of the SAME operand,
+//     X          =  D^{-1}       W[panel rows]          (16 x 16 x nrhs)
+//     W[trail]  +=  -(T D^{-1})  W[panel rows]          (kw x 16 x nrhs)
 // where D is the panel's 16 x 16 diagonal block of L (unit) or of U in
 // reversed coordinates (diagonal u_jj), T the band below it, and W the
-// window of active right-hand-side rows (shared memory, all columns).
+// window of active right-hand-side rows (shared memory, all columns).  With
+// T D^{-1} formed at setup both products are independent: every warp works
+// on its tiles at once and a panel costs one CTA barrier.
 // Row interchanges (forward sweep, ~0.2% of rows) are moved to the front of
 // their panel: the panel's swaps are applied to W first and the multiplier
 // columns carry the later in-panel swaps (getrf's convention), which is the
@@ -56,7 +58,7 @@ __device__ __forceinline__ void dmma_p(double (&d)[2], double a, double b) {
 }  // namespace
 
 // panel record: [D^{-1} fragments: 2 m-tiles x 4 k-steps x 32 lanes]
-//               [-T fragments: KWP/8 m-tiles x 4 k-steps x 32 lanes]
+//               [-(T D^{-1}) fragments: KWP/8 m-tiles x 4 k-steps x 32 lanes]
 //               [16 relative pivot rows (forward) / 0..15 (backward)]
 __host__ __device__ inline long long panel_doubles(int kwp) { return 256 + 16LL * kwp + 16; }
 
@@ -139,9 +141,12 @@ __global__ void __launch_bounds__(128) k_panel_convert(const LocalDesc* __restri
       const int f = e >> 5, lane = e & 31, mt = f >> 2, ks = f & 3;
       po[e] = X[(mt * 8 + (lane >> 2)) * 17 + ks * 4 + (lane & 3)];
     }
-    for (int e = tid; e < 16 * kwp; e += blockDim.x) {  // -T fragments
+    for (int e = tid; e < 16 * kwp; e += blockDim.x) {  // -(T D^{-1}) fragments
       const int f = e >> 5, lane = e & 31, mt = f >> 2, ks = f & 3;
-      po[256 + e] = -lt[(PB + mt * 8 + (lane >> 2)) * PB + ks * 4 + (lane & 3)];
+      const int r = PB + mt * 8 + (lane >> 2), c = ks * 4 + (lane & 3);
+      double acc = 0.0;
+      for (int k = 0; k < PB; ++k) acc = fma(lt[r * PB + k], X[k * 17 + c], acc);
+      po[256 + e] = -acc;
     }
     if (tid < PB) po[256 + 16 * kwp + tid] = (double)prel[tid];
     __syncthreads();
@@ -164,7 +169,7 @@ struct PanelArgs {
 
 template <bool FWD>
 __device__ __forceinline__ void panel_sweep(const PanelArgs& a, const LocalDesc& d, double* ring, uint64_t* full,
-                                            uint64_t* empty, double* W, double* Xb, int& chunk) {
+                                            uint64_t* empty, double* W, int& chunk) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = lane & 3, g = lane >> 2;
   const int n = d.n, kwp = FWD ? a.kwf : a.kwb, WR = a.WR;
   const int np = (n + PB - 1) / PB;
@@ -200,12 +205,14 @@ __device__ __forceinline__ void panel_sweep(const PanelArgs& a, const LocalDesc&
     const int stage = chunk % PNS;
     mbar_wait(&full[stage], (chunk / PNS) & 1);
     const double* rec = ring + (size_t)stage * a.stage_stride;
-    if (FWD) {  // the panel's row interchanges, moved to its front
-      const int pt = tid < PB ? __double2int_rn(rec[256 + 16 * kwp + tid]) : 0;
-      if (psync_or(tid < PB && pt != tid)) {
+    if (FWD) {  // the panel's row interchanges, moved to its front (every thread reads the same 16 pivots)
+      bool any = false;
+#pragma unroll
+      for (int t = 0; t < PB; ++t) any |= __double2int_rn(rec[256 + 16 * kwp + t]) != t;
+      if (any) {
         if (warp == 0) {
           for (int t = 0; t < PB; ++t) {
-            const int p2 = __shfl_sync(FULL, pt, t);
+            const int p2 = __double2int_rn(rec[256 + 16 * kwp + t]);
             if (p2 != t && lane < 16) {
               double* r1 = wrow(j0 + t);
               double* r2 = wrow(j0 + p2);
@@ -219,35 +226,59 @@ __device__ __forceinline__ void panel_sweep(const PanelArgs& a, const LocalDesc&
         psync();
       }
     }
-    // X = D^{-1} W[panel]: 2 x 2 output tiles on warps 0-3
-    if (warp < 4) {
-      const int mt = warp >> 1, nt = warp & 1;
-      double acc[2] = {0.0, 0.0};
+    // B fragments: the panel rows (the one operand of both products)
+    double bf[4][2];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const double* wr = wrow(j0 + ks * 4 + q);
+      bf[ks][0] = wr[g];
+      bf[ks][1] = wr[8 + g];
+    }
+    // tiles: 0..3 = X = D^{-1} W (2 m x 2 n), 4.. = trailing rows += -(T D^{-1}) W;
+    // warp w takes tiles w, w+8, ... in groups of TG with interleaved k-steps
+    const int ntile = 4 + 2 * mtT;
+    constexpr int TG = 5;
+    for (int t0 = warp; t0 < ntile; t0 += 8 * TG) {
+      double acc[TG][2];
+      double* crow[TG];
+#pragma unroll
+      for (int u = 0; u < TG; ++u) {
+        const int t = t0 + 8 * u;
+        acc[u][0] = acc[u][1] = 0.0;
+        crow[u] = nullptr;
+        if (t >= 4 && t < ntile) {
+          const int mt = (t - 4) >> 1, nt = (t - 4) & 1;
+          crow[u] = wrow(j0 + PB + mt * 8 + g) + nt * 8 + 2 * q;
+          const double2 c2 = *reinterpret_cast<const double2*>(crow[u]);
+          acc[u][0] = c2.x;
+          acc[u][1] = c2.y;
+        }
+      }
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
-        const double av = rec[(mt * 4 + ks) * 32 + lane];
-        const double bv = wrow(j0 + ks * 4 + q)[nt * 8 + g];
-        dmma_p(acc, av, bv);
+#pragma unroll
+        for (int u = 0; u < TG; ++u) {
+          const int t = t0 + 8 * u;
+          if (t < ntile) {
+            const int frag = t < 4 ? ((t >> 1) * 4 + ks) : 8 + ((t - 4) >> 1) * 4 + ks;
+            dmma_p(acc[u], rec[frag * 32 + lane], bf[ks][t < 4 ? (t & 1) : ((t - 4) & 1)]);
+          }
+        }
       }
-      const int r = mt * 8 + g, c = nt * 8 + 2 * q;
-      *reinterpret_cast<double2*>(Xb + r * PSR + c) = make_double2(acc[0], acc[1]);
-      out(j0 + r, c, acc[0]);
-      out(j0 + r, c + 1, acc[1]);
+#pragma unroll
+      for (int u = 0; u < TG; ++u) {
+        const int t = t0 + 8 * u;
+        if (t < 4) {
+          const int r = (t >> 1) * 8 + g, c = (t & 1) * 8 + 2 * q;
+          out(j0 + r, c, acc[u][0]);
+          out(j0 + r, c + 1, acc[u][1]);
+        } else if (t < ntile) {
+          *reinterpret_cast<double2*>(crow[u]) = make_double2(acc[u][0], acc[u][1]);
+        }
+      }
     }
     // entering rows take the slots of the previous panel (finished)
     wrow(erow)[ec] = evc;
-    psync();
-    // W[trail] += (-T) X: (kwp / 8) x 2 tiles over the 8 warps
-    const double* T = rec + 256;
-    for (int t = warp; t < 2 * mtT; t += 8) {
-      const int mt = t >> 1, nt = t & 1;
-      double* crow = wrow(j0 + PB + mt * 8 + g) + nt * 8 + 2 * q;
-      const double2 c2 = *reinterpret_cast<const double2*>(crow);
-      double acc[2] = {c2.x, c2.y};
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) dmma_p(acc, T[(mt * 4 + ks) * 32 + lane], Xb[(ks * 4 + q) * PSR + nt * 8 + g]);
-      *reinterpret_cast<double2*>(crow) = make_double2(acc[0], acc[1]);
-    }
     psync();
     if (tid == 0) mbar_arrive(&empty[stage]);
     ++chunk;
@@ -285,10 +316,9 @@ __global__ void __launch_bounds__(PTHREADS, 2) k_local_panel(PanelArgs a) {
     return;
   }
   double* W = sm + (size_t)PNS * a.stage_stride;
-  double* Xb = W + (size_t)a.WR * PSR;
   int chunk = 0;
-  panel_sweep<true>(a, d, sm, full, empty, W, Xb, chunk);
-  panel_sweep<false>(a, d, sm, full, empty, W, Xb, chunk);
+  panel_sweep<true>(a, d, sm, full, empty, W, chunk);
+  panel_sweep<false>(a, d, sm, full, empty, W, chunk);
 }
 
 // ------------------------------------------------------------------ host side
@@ -310,7 +340,7 @@ int launch_local_batch(HgPrecond* P, const double* R, long long ldr, int nrhs, c
 
 static size_t panel_smem(const HgPrecond* P) {
   const long long ss = std::max(panel_doubles(P->panel_kwf), panel_doubles(P->panel_kwb));
-  return sizeof(double) * ((size_t)PNS * ss + (size_t)P->panel_wr * PSR + (size_t)PB * PSR);
+  return sizeof(double) * ((size_t)PNS * ss + (size_t)P->panel_wr * PSR);
 }
 
 int launch_local_panel(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st) {

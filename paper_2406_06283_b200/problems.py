@@ -206,6 +206,11 @@ def _gevp_solve(forms, dec, method, n_wanted, i):
     return _coarse.solve_gevp_lanczos(g, n_wanted)
 
 
+def _tool_injected():
+    return any(k.startswith(("NV_NSIGHT_INJECTION", "NV_SANITIZER")) or k == "CUDA_INJECTION64_PATH"
+               for k in os.environ)
+
+
 def solve_local_gevps(forms, dec, method="auto", n_wanted=None, workers=None):
     """All coarse-subdomain eigenproblems; 'auto' = dense when every pencil is
     small (<= 2000 active dofs), Lanczos otherwise.  Runs in a fork pool."""
@@ -214,6 +219,10 @@ def solve_local_gevps(forms, dec, method="auto", n_wanted=None, workers=None):
     _G["args"] = (forms, dec, method, n_wanted)
     idx = list(range(dec.n_coarse))
     workers = workers or min(len(idx), os.cpu_count() or 1)
+    if _tool_injected():
+        # a fork of a process carrying a CUDA tool's injection (Nsight Compute,
+        # compute-sanitizer) crashes the tool with SIGSEGV: solve serially there
+        workers = 1
     try:
         if workers > 1 and len(idx) > 1:
             import multiprocessing as mp
