@@ -167,121 +167,155 @@ struct PanelArgs {
   int nrhs, kwf, kwb, WR, stage_stride;
 };
 
+struct PanelSweep {
+  const PanelArgs* a;
+  const int* idx;
+  double* xs;
+  double* W;
+  const double* ring;
+  uint64_t* full;
+  uint64_t* empty;
+  int n, kwp, WR, mtT;
+  int* chunk;
+};
+
+template <bool FWD>
+__device__ __forceinline__ double panel_in(const PanelSweep& S, int row, int c) {
+  if (row >= S.n || c >= S.a->nrhs) return 0.0;
+  if (FWD) return __ldg(S.a->R + (long long)c * S.a->ldr + __ldg(S.idx + row));
+  return S.xs[(long long)c * S.a->xs_len + (S.n - 1 - row)];
+}
+
+// window row (j0 + off) for 0 <= off < WR, given base = j0 mod WR
+__device__ __forceinline__ double* panel_row(const PanelSweep& S, int base, int off) {
+  int r = base + off;
+  if (r >= S.WR) r -= S.WR;
+  return S.W + (size_t)r * PSR;
+}
+
+// One panel p.  `ev` is this panel's slot of the entering-row look-ahead: it
+// holds the value loaded PD panels ago (stored into the window here) and is
+// refilled for panel p + PD — a fixed register per slot (the caller unrolls
+// PD panels), so no in-flight load is ever moved between registers.
+template <bool FWD>
+__device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& ev) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = lane & 3, g = lane >> 2;
+  const int er = tid >> 4, ec = tid & 15;
+  const int kwp = S.kwp;
+  const int j0 = p * PB;
+  const int base = j0 % S.WR;
+  const double evc = ev;
+  ev = panel_in<FWD>(S, j0 + PB + kwp + er + PB * PD, ec);
+  const int chunk = *S.chunk;
+  const int stage = chunk % PNS;
+  mbar_wait(&S.full[stage], (chunk / PNS) & 1);
+  const double* rec = S.ring + (size_t)stage * S.a->stage_stride;
+  if (FWD) {  // the panel's row interchanges, moved to its front (every thread reads the same 16 pivots)
+    bool any = false;
+#pragma unroll
+    for (int t = 0; t < PB; ++t) any |= __double2int_rn(rec[256 + 16 * kwp + t]) != t;
+    if (any) {
+      if (warp == 0) {
+        for (int t = 0; t < PB; ++t) {
+          const int p2 = __double2int_rn(rec[256 + 16 * kwp + t]);
+          if (p2 != t && lane < 16) {
+            double* r1 = panel_row(S, base, t);
+            double* r2 = panel_row(S, base, p2);
+            const double tmp = r1[lane];
+            r1[lane] = r2[lane];
+            r2[lane] = tmp;
+          }
+          __syncwarp();
+        }
+      }
+      psync();
+    }
+  }
+  // B fragments: the panel rows (the one operand of both products)
+  double b0[4], b1[4];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const double* wr = panel_row(S, base, ks * 4 + q);
+    b0[ks] = wr[g];
+    b1[ks] = wr[8 + g];
+  }
+  // tiles: 0..3 = X = D^{-1} W (2 m x 2 n); 4.. = trailing rows += -(T D^{-1}) W.
+  // Warp w takes tiles w, w+8, ... in groups of TG with interleaved k-steps.
+  const int ntile = 4 + 2 * S.mtT;
+  constexpr int TG = 5;
+  for (int t0 = warp; t0 < ntile; t0 += 8 * TG) {
+    double acc[TG][2];
+    double* crow[TG];
+#pragma unroll
+    for (int u = 0; u < TG; ++u) {
+      const int t = t0 + 8 * u;
+      acc[u][0] = acc[u][1] = 0.0;
+      crow[u] = nullptr;
+      if (t >= 4 && t < ntile) {
+        const int mt = (t - 4) >> 1, nt = (t - 4) & 1;
+        crow[u] = panel_row(S, base, PB + mt * 8 + g) + nt * 8 + 2 * q;
+        const double2 c2 = *reinterpret_cast<const double2*>(crow[u]);
+        acc[u][0] = c2.x;
+        acc[u][1] = c2.y;
+      }
+    }
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+      for (int u = 0; u < TG; ++u) {
+        const int t = t0 + 8 * u;  // t0 and warp share parity: the n-tile is (t & 1) for every tile
+        if (t < ntile) {
+          const int frag = t < 4 ? ((t >> 1) * 4 + ks) : 8 + ((t - 4) >> 1) * 4 + ks;
+          dmma_p(acc[u], rec[frag * 32 + lane], (t & 1) ? b1[ks] : b0[ks]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < TG; ++u) {
+      const int t = t0 + 8 * u;
+      if (t < 4) {
+        const int r = (t >> 1) * 8 + g, c = (t & 1) * 8 + 2 * q;
+        double* xs = S.xs + (FWD ? (long long)(j0 + r) : (long long)(S.n - 1 - (j0 + r)));
+        if (j0 + r < S.n) {
+          if (c < S.a->nrhs) xs[(long long)c * S.a->xs_len] = acc[u][0];
+          if (c + 1 < S.a->nrhs) xs[(long long)(c + 1) * S.a->xs_len] = acc[u][1];
+        }
+      } else if (t < ntile) {
+        *reinterpret_cast<double2*>(crow[u]) = make_double2(acc[u][0], acc[u][1]);
+      }
+    }
+  }
+  // entering rows take the slots of the previous panel (finished)
+  panel_row(S, base, PB + kwp + er)[ec] = evc;
+  psync();
+  if (tid == 0) mbar_arrive(&S.empty[stage]);
+  *S.chunk = chunk + 1;
+}
+
 template <bool FWD>
 __device__ __forceinline__ void panel_sweep(const PanelArgs& a, const LocalDesc& d, double* ring, uint64_t* full,
                                             uint64_t* empty, double* W, int& chunk) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = lane & 3, g = lane >> 2;
-  const int n = d.n, kwp = FWD ? a.kwf : a.kwb, WR = a.WR;
-  const int np = (n + PB - 1) / PB;
-  const int* idx = a.idx + d.idx_off;
-  double* xs = a.xs + d.idx_off;
-  auto in = [&](int row, int c) -> double {
-    if (row >= n || c >= a.nrhs) return 0.0;
-    if (FWD) return __ldg(a.R + (long long)c * a.ldr + __ldg(idx + row));
-    return xs[(long long)c * a.xs_len + (n - 1 - row)];
-  };
-  auto out = [&](int row, int c, double v) {
-    if (row < n && c < a.nrhs) xs[(long long)c * a.xs_len + (FWD ? row : n - 1 - row)] = v;
-  };
-  auto wrow = [&](int row) -> double* { return W + (size_t)(row % WR) * PSR; };
+  const int tid = threadIdx.x;
+  PanelSweep S{&a, a.idx + d.idx_off, a.xs + d.idx_off, W, ring, full, empty, d.n, FWD ? a.kwf : a.kwb, a.WR, 0,
+               &chunk};
+  S.mtT = S.kwp >> 3;
+  const int np = (S.n + PB - 1) / PB;
   // prologue: panel 0 and its trailing rows
-  for (int e = tid; e < (PB + kwp) * 16; e += 256) wrow(e >> 4)[e & 15] = in(e >> 4, e & 15);
+  for (int e = tid; e < (PB + S.kwp) * 16; e += 256) panel_row(S, 0, e >> 4)[e & 15] = panel_in<FWD>(S, e >> 4, e & 15);
   // rows entering at panels 0..PD-1, in flight ahead of their use (this
   // thread's row tid / 16, column tid % 16 of each 16-row group)
   const int er = tid >> 4, ec = tid & 15;
-  double ev[PD];
-#pragma unroll
-  for (int k = 0; k < PD; ++k) ev[k] = in(PB + kwp + PB * k + er, ec);
+  double ev0 = panel_in<FWD>(S, PB + S.kwp + er, ec);
+  double ev1 = panel_in<FWD>(S, PB + S.kwp + PB + er, ec);
+  double ev2 = panel_in<FWD>(S, PB + S.kwp + 2 * PB + er, ec);
+  double ev3 = panel_in<FWD>(S, PB + S.kwp + 3 * PB + er, ec);
+  static_assert(PD == 4, "unrolled look-ahead slots");
   psync();
-  const int mtT = kwp >> 3;
-  for (int p = 0; p < np; ++p) {
-    const int j0 = p * PB;
-    // rows entering for the next panel's trailing update (loaded PD panels ago)
-    const int erow = j0 + PB + kwp + er;
-    const double evc = ev[0];
-#pragma unroll
-    for (int k = 0; k + 1 < PD; ++k) ev[k] = ev[k + 1];
-    ev[PD - 1] = in(erow + PB * PD, ec);
-    const int stage = chunk % PNS;
-    mbar_wait(&full[stage], (chunk / PNS) & 1);
-    const double* rec = ring + (size_t)stage * a.stage_stride;
-    if (FWD) {  // the panel's row interchanges, moved to its front (every thread reads the same 16 pivots)
-      bool any = false;
-#pragma unroll
-      for (int t = 0; t < PB; ++t) any |= __double2int_rn(rec[256 + 16 * kwp + t]) != t;
-      if (any) {
-        if (warp == 0) {
-          for (int t = 0; t < PB; ++t) {
-            const int p2 = __double2int_rn(rec[256 + 16 * kwp + t]);
-            if (p2 != t && lane < 16) {
-              double* r1 = wrow(j0 + t);
-              double* r2 = wrow(j0 + p2);
-              const double tmp = r1[lane];
-              r1[lane] = r2[lane];
-              r2[lane] = tmp;
-            }
-            __syncwarp();
-          }
-        }
-        psync();
-      }
-    }
-    // B fragments: the panel rows (the one operand of both products)
-    double bf[4][2];
-#pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      const double* wr = wrow(j0 + ks * 4 + q);
-      bf[ks][0] = wr[g];
-      bf[ks][1] = wr[8 + g];
-    }
-    // tiles: 0..3 = X = D^{-1} W (2 m x 2 n), 4.. = trailing rows += -(T D^{-1}) W;
-    // warp w takes tiles w, w+8, ... in groups of TG with interleaved k-steps
-    const int ntile = 4 + 2 * mtT;
-    constexpr int TG = 5;
-    for (int t0 = warp; t0 < ntile; t0 += 8 * TG) {
-      double acc[TG][2];
-      double* crow[TG];
-#pragma unroll
-      for (int u = 0; u < TG; ++u) {
-        const int t = t0 + 8 * u;
-        acc[u][0] = acc[u][1] = 0.0;
-        crow[u] = nullptr;
-        if (t >= 4 && t < ntile) {
-          const int mt = (t - 4) >> 1, nt = (t - 4) & 1;
-          crow[u] = wrow(j0 + PB + mt * 8 + g) + nt * 8 + 2 * q;
-          const double2 c2 = *reinterpret_cast<const double2*>(crow[u]);
-          acc[u][0] = c2.x;
-          acc[u][1] = c2.y;
-        }
-      }
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-#pragma unroll
-        for (int u = 0; u < TG; ++u) {
-          const int t = t0 + 8 * u;
-          if (t < ntile) {
-            const int frag = t < 4 ? ((t >> 1) * 4 + ks) : 8 + ((t - 4) >> 1) * 4 + ks;
-            dmma_p(acc[u], rec[frag * 32 + lane], bf[ks][t < 4 ? (t & 1) : ((t - 4) & 1)]);
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < TG; ++u) {
-        const int t = t0 + 8 * u;
-        if (t < 4) {
-          const int r = (t >> 1) * 8 + g, c = (t & 1) * 8 + 2 * q;
-          out(j0 + r, c, acc[u][0]);
-          out(j0 + r, c + 1, acc[u][1]);
-        } else if (t < ntile) {
-          *reinterpret_cast<double2*>(crow[u]) = make_double2(acc[u][0], acc[u][1]);
-        }
-      }
-    }
-    // entering rows take the slots of the previous panel (finished)
-    wrow(erow)[ec] = evc;
-    psync();
-    if (tid == 0) mbar_arrive(&empty[stage]);
-    ++chunk;
+  for (int p = 0; p < np; p += PD) {
+    panel_step<FWD>(S, p, ev0);
+    if (p + 1 < np) panel_step<FWD>(S, p + 1, ev1);
+    if (p + 2 < np) panel_step<FWD>(S, p + 2, ev2);
+    if (p + 3 < np) panel_step<FWD>(S, p + 3, ev3);
   }
 }
 
