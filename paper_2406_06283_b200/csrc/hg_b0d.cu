@@ -80,22 +80,17 @@ __global__ void k_creduce_multi(int m, int nrhs, const int* __restrict__ col_blk
 }
 
 // Y_slice[s] (64-row panel of this CTA) = B0^{-1}[rows, k in slice s] * C[k in slice s, :]
-// 8 warps x 8 rows, 2 DMMA accumulators (16 columns) per warp.  The k index
-// of a DMMA step is permuted (lane q takes k = kc + q KCH/4 + ks, B uses the
-// same permutation), so each lane streams its row segment with 16-byte loads,
-// 8 in flight, instead of one 8-byte load per step.
+// 8 warps x 8 rows, 2 DMMA accumulators (16 columns) per warp.
 __global__ void __launch_bounds__(256) k_b0_gemm_multi(int m, const double* __restrict__ Binv,
                                                        const double* __restrict__ C, double* __restrict__ Yp) {
   __shared__ __align__(16) double s_c[KCH * SRD];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, g = lane >> 2;
   const int r0 = blockIdx.x * 64 + warp * 8;
   const int slice = blockIdx.y;
-  const int klen = ((m + B0_KSPLIT - 1) / B0_KSPLIT + 1) & ~1;  // even: 16-byte aligned segments
+  const int klen = (m + B0_KSPLIT - 1) / B0_KSPLIT;
   const int ka = slice * klen, kb = min(m, ka + klen);
   const int row = r0 + g;
   const double* arow = Binv + (size_t)min(row, m - 1) * m;
-  const bool vec = (m & 1) == 0;  // rows 16-byte aligned
-  constexpr int KQ = KCH / 4;     // k per lane per chunk
   double acc0[2] = {0.0, 0.0}, acc1[2] = {0.0, 0.0};
   for (int kc = ka; kc < kb; kc += KCH) {
     const int kn = min(KCH, kb - kc);
@@ -105,31 +100,12 @@ __global__ void __launch_bounds__(256) k_b0_gemm_multi(int m, const double* __re
       s_c[k * SRD + col] = k < kn ? C[(size_t)(kc + k) * MRD + col] : 0.0;
     }
     __syncthreads();
-    const int kq0 = q * KQ;  // this lane's k segment within the chunk
-#pragma unroll 1
-    for (int ks0 = 0; ks0 < KQ; ks0 += 16) {
-      double av[16];
-      if (vec && row < m && kq0 + ks0 + 16 <= kn) {
-        const double2* ap = reinterpret_cast<const double2*>(arow + kc + kq0 + ks0);
-#pragma unroll
-        for (int h = 0; h < 8; ++h) {
-          const double2 t = __ldg(ap + h);
-          av[2 * h] = t.x;
-          av[2 * h + 1] = t.y;
-        }
-      } else {
-#pragma unroll
-        for (int h = 0; h < 16; ++h) {
-          const int k = kq0 + ks0 + h;
-          av[h] = (row < m && k < kn) ? __ldg(arow + kc + k) : 0.0;
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < 16; ++h) {
-        const int k = kq0 + ks0 + h;  // B row of this step for lane q (k < kn: s_c is zero padded)
-        dmma_d(acc0, av[h], s_c[k * SRD + g]);
-        dmma_d(acc1, av[h], s_c[k * SRD + 8 + g]);
-      }
+#pragma unroll 8
+    for (int ks = 0; ks < KCH; ks += 4) {
+      const int k = ks + q;
+      const double a = (row < m && k < kn) ? __ldg(arow + kc + k) : 0.0;
+      dmma_d(acc0, a, s_c[k * SRD + g]);
+      dmma_d(acc1, a, s_c[k * SRD + 8 + g]);
     }
   }
   if (row < m) {

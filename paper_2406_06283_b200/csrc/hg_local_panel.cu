@@ -186,6 +186,17 @@ __device__ __forceinline__ double panel_in(const PanelSweep& S, int row, int c) 
   return S.xs[(long long)c * S.a->xs_len + (S.n - 1 - row)];
 }
 
+// the gather split in two: the index (loaded a further PD panels ahead, so
+// that the value load never waits on it) and the value
+__device__ __forceinline__ int panel_idx(const PanelSweep& S, int row) { return row < S.n ? __ldg(S.idx + row) : -1; }
+
+template <bool FWD>
+__device__ __forceinline__ double panel_val(const PanelSweep& S, int row, int c, int gi) {
+  if (row >= S.n || c >= S.a->nrhs) return 0.0;
+  if (FWD) return __ldg(S.a->R + (long long)c * S.a->ldr + gi);
+  return S.xs[(long long)c * S.a->xs_len + (S.n - 1 - row)];
+}
+
 // window row (j0 + off) for 0 <= off < WR, given base = j0 mod WR
 __device__ __forceinline__ double* panel_row(const PanelSweep& S, int base, int off) {
   int r = base + off;
@@ -198,22 +209,28 @@ __device__ __forceinline__ double* panel_row(const PanelSweep& S, int base, int 
 // refilled for panel p + PD — a fixed register per slot (the caller unrolls
 // PD panels), so no in-flight load is ever moved between registers.
 template <bool FWD>
-__device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& ev) {
+__device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& ev, int& ei) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = lane & 3, g = lane >> 2;
   const int er = tid >> 4, ec = tid & 15;
   const int kwp = S.kwp;
   const int j0 = p * PB;
   const int base = j0 % S.WR;
   const double evc = ev;
-  ev = panel_in<FWD>(S, j0 + PB + kwp + er + PB * PD, ec);
+  const int erow = j0 + PB + kwp + er;
+  ev = panel_val<FWD>(S, erow + PB * PD, ec, ei);       // value for panel p + PD (its index loaded PD panels ago)
+  if (FWD) ei = panel_idx(S, erow + 2 * PB * PD);       // index for panel p + 2 PD
   const int chunk = *S.chunk;
   const int stage = chunk % PNS;
   mbar_wait(&S.full[stage], (chunk / PNS) & 1);
   const double* rec = S.ring + (size_t)stage * S.a->stage_stride;
   if (FWD) {  // the panel's row interchanges, moved to its front (every thread reads the same 16 pivots)
     bool any = false;
+    const double2* pv = reinterpret_cast<const double2*>(rec + 256 + 16 * kwp);
 #pragma unroll
-    for (int t = 0; t < PB; ++t) any |= __double2int_rn(rec[256 + 16 * kwp + t]) != t;
+    for (int t = 0; t < PB / 2; ++t) {
+      const double2 v = pv[t];
+      any |= (v.x != (double)(2 * t)) | (v.y != (double)(2 * t + 1));
+    }
     if (any) {
       if (warp == 0) {
         for (int t = 0; t < PB; ++t) {
@@ -240,49 +257,53 @@ __device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& e
     b1[ks] = wr[8 + g];
   }
   // tiles: 0..3 = X = D^{-1} W (2 m x 2 n); 4.. = trailing rows += -(T D^{-1}) W.
-  // Warp w takes tiles w, w+8, ... in groups of TG with interleaved k-steps.
+  // Warp w takes tiles w, w+8, ... (all of the same n-tile, w & 1), at most
+  // TG of them, k-steps interleaved across its tiles.
   const int ntile = 4 + 2 * S.mtT;
   constexpr int TG = 5;
-  for (int t0 = warp; t0 < ntile; t0 += 8 * TG) {
-    double acc[TG][2];
-    double* crow[TG];
+  const int nu = (ntile - warp + 7) >> 3;  // tiles of this warp (<= TG: ntile <= 40)
+  const double* bsel = (warp & 1) ? b1 : b0;
+  double acc[TG][2];
+  const double* ap[TG];
+  double* crow[TG];
 #pragma unroll
-    for (int u = 0; u < TG; ++u) {
-      const int t = t0 + 8 * u;
-      acc[u][0] = acc[u][1] = 0.0;
-      crow[u] = nullptr;
-      if (t >= 4 && t < ntile) {
-        const int mt = (t - 4) >> 1, nt = (t - 4) & 1;
-        crow[u] = panel_row(S, base, PB + mt * 8 + g) + nt * 8 + 2 * q;
+  for (int u = 0; u < TG; ++u) {
+    const int t = warp + 8 * u;
+    acc[u][0] = acc[u][1] = 0.0;
+    crow[u] = nullptr;
+    ap[u] = rec + lane;
+    if (u < nu) {
+      if (t < 4) {
+        ap[u] = rec + (t >> 1) * 128 + lane;
+      } else {
+        const int mt = (t - 4) >> 1;
+        ap[u] = rec + 256 + mt * 128 + lane;
+        crow[u] = panel_row(S, base, PB + mt * 8 + g) + (t & 1) * 8 + 2 * q;
         const double2 c2 = *reinterpret_cast<const double2*>(crow[u]);
         acc[u][0] = c2.x;
         acc[u][1] = c2.y;
       }
     }
+  }
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
+  for (int ks = 0; ks < 4; ++ks) {
 #pragma unroll
-      for (int u = 0; u < TG; ++u) {
-        const int t = t0 + 8 * u;  // t0 and warp share parity: the n-tile is (t & 1) for every tile
-        if (t < ntile) {
-          const int frag = t < 4 ? ((t >> 1) * 4 + ks) : 8 + ((t - 4) >> 1) * 4 + ks;
-          dmma_p(acc[u], rec[frag * 32 + lane], (t & 1) ? b1[ks] : b0[ks]);
-        }
+    for (int u = 0; u < TG; ++u)
+      if (u < nu) dmma_p(acc[u], ap[u][ks * 32], bsel[ks]);
+  }
+#pragma unroll
+  for (int u = 0; u < TG; ++u) {
+    if (u >= nu) continue;
+    const int t = warp + 8 * u;
+    if (t < 4) {
+      const int r = (t >> 1) * 8 + g, c = (t & 1) * 8 + 2 * q;
+      double* xs = S.xs + (FWD ? (long long)(j0 + r) : (long long)(S.n - 1 - (j0 + r)));
+      if (j0 + r < S.n) {
+        if (c < S.a->nrhs) xs[(long long)c * S.a->xs_len] = acc[u][0];
+        if (c + 1 < S.a->nrhs) xs[(long long)(c + 1) * S.a->xs_len] = acc[u][1];
       }
-    }
-#pragma unroll
-    for (int u = 0; u < TG; ++u) {
-      const int t = t0 + 8 * u;
-      if (t < 4) {
-        const int r = (t >> 1) * 8 + g, c = (t & 1) * 8 + 2 * q;
-        double* xs = S.xs + (FWD ? (long long)(j0 + r) : (long long)(S.n - 1 - (j0 + r)));
-        if (j0 + r < S.n) {
-          if (c < S.a->nrhs) xs[(long long)c * S.a->xs_len] = acc[u][0];
-          if (c + 1 < S.a->nrhs) xs[(long long)(c + 1) * S.a->xs_len] = acc[u][1];
-        }
-      } else if (t < ntile) {
-        *reinterpret_cast<double2*>(crow[u]) = make_double2(acc[u][0], acc[u][1]);
-      }
+    } else {
+      *reinterpret_cast<double2*>(crow[u]) = make_double2(acc[u][0], acc[u][1]);
     }
   }
   // entering rows take the slots of the previous panel (finished)
@@ -305,17 +326,25 @@ __device__ __forceinline__ void panel_sweep(const PanelArgs& a, const LocalDesc&
   // rows entering at panels 0..PD-1, in flight ahead of their use (this
   // thread's row tid / 16, column tid % 16 of each 16-row group)
   const int er = tid >> 4, ec = tid & 15;
-  double ev0 = panel_in<FWD>(S, PB + S.kwp + er, ec);
-  double ev1 = panel_in<FWD>(S, PB + S.kwp + PB + er, ec);
-  double ev2 = panel_in<FWD>(S, PB + S.kwp + 2 * PB + er, ec);
-  double ev3 = panel_in<FWD>(S, PB + S.kwp + 3 * PB + er, ec);
+  const int r0 = PB + S.kwp + er;
+  double ev0 = panel_in<FWD>(S, r0, ec);
+  double ev1 = panel_in<FWD>(S, r0 + PB, ec);
+  double ev2 = panel_in<FWD>(S, r0 + 2 * PB, ec);
+  double ev3 = panel_in<FWD>(S, r0 + 3 * PB, ec);
+  int ei0 = 0, ei1 = 0, ei2 = 0, ei3 = 0;  // gather indices of panels 4..7 (forward sweep)
+  if (FWD) {
+    ei0 = panel_idx(S, r0 + 4 * PB);
+    ei1 = panel_idx(S, r0 + 5 * PB);
+    ei2 = panel_idx(S, r0 + 6 * PB);
+    ei3 = panel_idx(S, r0 + 7 * PB);
+  }
   static_assert(PD == 4, "unrolled look-ahead slots");
   psync();
   for (int p = 0; p < np; p += PD) {
-    panel_step<FWD>(S, p, ev0);
-    if (p + 1 < np) panel_step<FWD>(S, p + 1, ev1);
-    if (p + 2 < np) panel_step<FWD>(S, p + 2, ev2);
-    if (p + 3 < np) panel_step<FWD>(S, p + 3, ev3);
+    panel_step<FWD>(S, p, ev0, ei0);
+    if (p + 1 < np) panel_step<FWD>(S, p + 1, ev1, ei1);
+    if (p + 2 < np) panel_step<FWD>(S, p + 2, ev2, ei2);
+    if (p + 3 < np) panel_step<FWD>(S, p + 3, ev3, ei3);
   }
 }
 
