@@ -35,7 +35,7 @@ namespace hg {
 namespace {
 constexpr int PB = 16;        // panel rows
 constexpr int PSR = 20;       // window row stride (16 columns + pad: conflict-free B fragments)
-constexpr int PNS = 4;        // ring stages
+constexpr int PNS_MAX = 8;    // ring stages (runtime count ns <= PNS_MAX: PanelArgs::ns)
 constexpr int PD = 4;         // panels of look-ahead for the entering rows (a gather is two dependent loads)
 constexpr int PTHREADS = 256 + 32;
 
@@ -164,7 +164,7 @@ struct PanelArgs {
   long long ldr;
   double* xs;
   long long xs_len;
-  int nrhs, kwf, kwb, WR, stage_stride;
+  int nrhs, kwf, kwb, WR, stage_stride, ns;
 };
 
 struct PanelSweep {
@@ -220,8 +220,9 @@ __device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& e
   ev = panel_val<FWD>(S, erow + PB * PD, ec, ei);       // value for panel p + PD (its index loaded PD panels ago)
   if (FWD) ei = panel_idx(S, erow + 2 * PB * PD);       // index for panel p + 2 PD
   const int chunk = *S.chunk;
-  const int stage = chunk % PNS;
-  mbar_wait(&S.full[stage], (chunk / PNS) & 1);
+  const int ns = S.a->ns;
+  const int stage = chunk % ns;
+  mbar_wait(&S.full[stage], (chunk / ns) & 1);
   const double* rec = S.ring + (size_t)stage * S.a->stage_stride;
   if (FWD) {  // the panel's row interchanges, moved to its front (every thread reads the same 16 pivots)
     bool any = false;
@@ -350,10 +351,11 @@ __device__ __forceinline__ void panel_sweep(const PanelArgs& a, const LocalDesc&
 
 __global__ void __launch_bounds__(PTHREADS, 2) k_local_panel(PanelArgs a) {
   extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) uint64_t full[PNS], empty[PNS];
+  __shared__ __align__(8) uint64_t full[PNS_MAX], empty[PNS_MAX];
+  const int ns = a.ns;
   const LocalDesc d = a.descs[blockIdx.x];
   if (threadIdx.x == 0) {
-    for (int s = 0; s < PNS; ++s) {
+    for (int s = 0; s < ns; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -366,8 +368,8 @@ __global__ void __launch_bounds__(PTHREADS, 2) k_local_panel(PanelArgs a) {
     if (threadIdx.x == 256) {  // producer: forward panels, then backward panels
       const long long psf = panel_doubles(a.kwf), psb = panel_doubles(a.kwb);
       for (int c = 0; c < 2 * np; ++c) {
-        const int stage = c % PNS;
-        if (c >= PNS) mbar_wait(&empty[stage], ((c / PNS) - 1) & 1);
+        const int stage = c % ns;
+        if (c >= ns) mbar_wait(&empty[stage], ((c / ns) - 1) & 1);
         const bool f = c < np;
         const int pp = f ? c : c - np;
         const double* src = f ? a.pf + a.poff[2 * blockIdx.x] + pp * psf : a.pb + a.poff[2 * blockIdx.x + 1] + pp * psb;
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(PTHREADS, 2) k_local_panel(PanelArgs a) {
     }
     return;
   }
-  double* W = sm + (size_t)PNS * a.stage_stride;
+  double* W = sm + (size_t)ns * a.stage_stride;
   int chunk = 0;
   panel_sweep<true>(a, d, sm, full, empty, W, chunk);
   panel_sweep<false>(a, d, sm, full, empty, W, chunk);
@@ -401,9 +403,20 @@ int launch_local_batch(HgPrecond* P, const double* R, long long ldr, int nrhs, c
   return launch_local_solve_multi(P, R, ldr, nrhs, st);
 }
 
+// ring stages: as many as fit beside the window with two CTAs per SM (at least
+// 3), HG_PANEL_STAGES overrides (up to PNS_MAX; experiments)
+static int panel_stages(const HgPrecond* P) {
+  const long long ss = std::max(panel_doubles(P->panel_kwf), panel_doubles(P->panel_kwb)) * 8;
+  const long long win = (long long)P->panel_wr * PSR * 8;
+  static const int env = getenv("HG_PANEL_STAGES") ? atoi(getenv("HG_PANEL_STAGES")) : 0;
+  if (env > 0) return std::min(env, PNS_MAX);
+  const long long budget = 113 * 1024 - 256;  // two CTAs per SM
+  return (int)std::max(3LL, std::min((long long)PNS_MAX, (budget - win) / ss));
+}
+
 static size_t panel_smem(const HgPrecond* P) {
   const long long ss = std::max(panel_doubles(P->panel_kwf), panel_doubles(P->panel_kwb));
-  return sizeof(double) * ((size_t)PNS * ss + (size_t)P->panel_wr * PSR);
+  return sizeof(double) * ((size_t)panel_stages(P) * ss + (size_t)P->panel_wr * PSR);
 }
 
 int launch_local_panel(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st) {
@@ -412,7 +425,7 @@ int launch_local_panel(HgPrecond* P, const double* R, long long ldr, int nrhs, c
   HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k_local_panel), smem, false));
   PanelArgs a{P->d_local, P->d_poff, P->d_local_idx, P->d_pfwd, P->d_pbwd, R, ldr, P->d_xsm, P->xs_len, nrhs,
               P->panel_kwf, P->panel_kwb, P->panel_wr,
-              (int)std::max(panel_doubles(P->panel_kwf), panel_doubles(P->panel_kwb))};
+              (int)std::max(panel_doubles(P->panel_kwf), panel_doubles(P->panel_kwb)), panel_stages(P)};
   k_local_panel<<<P->n_local, PTHREADS, smem, st>>>(a);
   HG_LAUNCH_CHECK();
   return HG_OK;
