@@ -221,9 +221,12 @@ int hg_precond_read(HgPrecond* p, int32_t field, double* host, int64_t count);
  *   HG_STAT_PANEL_DEVIATION  its check against the row solve on a seeded
  *                            16-column batch: max over columns of
  *                            max|x_panel - x_row| / max|x_row| (must be
- *                            <= 1e-11 to be active; -1 = not built) */
+ *                            <= 1e-11 to be active; -1 = not built)
+ *   HG_STAT_PANEL_BYTES      panel-record bytes one batched local solve
+ *                            streams (each panel's nonzero part only) */
 #define HG_STAT_PANEL_ACTIVE 1
 #define HG_STAT_PANEL_DEVIATION 2
+#define HG_STAT_PANEL_BYTES 3  /* factor bytes one batched local solve streams */
 double hg_precond_stat(HgPrecond* p, int32_t key);
 /* out = M^{-1} r ; r, out: device, length n; out fully overwritten. */
 int hg_precond_apply(HgPrecond* p, const double* r, double* out, void* stream);

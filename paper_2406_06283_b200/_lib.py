@@ -129,7 +129,7 @@ SIGNATURES = {
     "hg_precond_read": (ctypes.c_int, [_vp, ctypes.c_int32, _f64p, ctypes.c_int64]),
     "hg_precond_stat": (ctypes.c_double, [_vp, ctypes.c_int32]),
 }
-STAT_PANEL_ACTIVE, STAT_PANEL_DEVIATION = 1, 2
+STAT_PANEL_ACTIVE, STAT_PANEL_DEVIATION, STAT_PANEL_BYTES = 1, 2, 3
 FIELD_LOCAL_FWD, FIELD_LOCAL_BWD = 1, 2
 
 ABI_VERSION = 3

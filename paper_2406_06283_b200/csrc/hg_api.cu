@@ -754,6 +754,8 @@ int hg_precond_destroy(HgPrecond* P) {
   release(P->d_poff);
   release(P->d_pfwd);
   release(P->d_pbwd);
+  release(P->d_pmt);
+  release(P->d_mtoff);
   release(P->d_xs);
   release(P->d_lptr);
   release(P->d_lent);
@@ -1280,6 +1282,8 @@ double hg_precond_stat(HgPrecond* P, int32_t key) {
       return P->panel_ok ? 1.0 : 0.0;
     case HG_STAT_PANEL_DEVIATION:
       return P->panel_dev;
+    case HG_STAT_PANEL_BYTES:
+      return (double)P->panel_stream_bytes;
     default:
       return NAN;
   }

@@ -50,7 +50,10 @@ struct HgPrecond {
   long long* d_poff = nullptr;    // [2 n_local] forward / backward panel offsets
   double* d_pfwd = nullptr;
   double* d_pbwd = nullptr;
-  int panel_kwf = 0, panel_kwb = 0, panel_wr = 0;
+  int panel_kwf = 0, panel_kwb = 0, panel_wr = 0, panel_np_max = 0;
+  unsigned char* d_pmt = nullptr;    // per panel: nonzero 8-row tiles of its trailing block
+  long long* d_mtoff = nullptr;      // [n_local]: block s's counts (forward, then backward)
+  long long panel_stream_bytes = 0;  // factor bytes one batched local solve streams
   bool panel_ok = false;          // panel records built and checked against the row solve
   double panel_dev = -1.0;        // that check's deviation (-1: not built)
   long long xs_len = 0;

@@ -57,10 +57,16 @@ __device__ __forceinline__ void dmma_p(double (&d)[2], double a, double b) {
 }
 }  // namespace
 
-// panel record: [D^{-1} fragments: 2 m-tiles x 4 k-steps x 32 lanes]
+// panel record: [16 relative pivot rows (forward) / 0..15 (backward)]
+//               [D^{-1} fragments: 2 m-tiles x 4 k-steps x 32 lanes]
 //               [-(T D^{-1}) fragments: KWP/8 m-tiles x 4 k-steps x 32 lanes]
-//               [16 relative pivot rows (forward) / 0..15 (backward)]
-__host__ __device__ inline long long panel_doubles(int kwp) { return 256 + 16LL * kwp + 16; }
+// in a fixed stride; only the first 272 + 128 mt doubles are streamed, mt =
+// the panel's count of nonzero 8-row m-tiles of T (per-panel byte `pmt`):
+// U's band reaches kl + ku only below row interchanges, so most backward
+// panels need about half of KWP.
+constexpr int PREC_HDR = 16 + 256;  // pivots + D^{-1} fragments (doubles)
+__host__ __device__ inline long long panel_doubles(int kwp) { return PREC_HDR + 16LL * kwp; }
+__host__ __device__ inline long long panel_used(int mt) { return PREC_HDR + 128LL * mt; }
 
 // ------------------------------------------------------------------ setup conversion
 // One CTA per block, 128 threads, panels in order.  Lt[(16 + KWP) x 16]: the
@@ -70,7 +76,9 @@ template <bool FWD>
 __global__ void __launch_bounds__(128) k_panel_convert(const LocalDesc* __restrict__ descs,
                                                        const double* __restrict__ rec_all,
                                                        const long long* __restrict__ poff, int kwp,
-                                                       double* __restrict__ out_all) {
+                                                       double* __restrict__ out_all,
+                                                       const long long* __restrict__ mtoff,
+                                                       unsigned char* __restrict__ mt_all) {
   extern __shared__ double lt[];  // (16 + kwp) x 16, then dinvd[16], then X[16][17]
   const LocalDesc d = descs[blockIdx.x];
   const int n = d.n;
@@ -137,18 +145,26 @@ __global__ void __launch_bounds__(128) k_panel_convert(const LocalDesc* __restri
     }
     __syncthreads();
     double* po = out + (long long)p * PS;
+    if (tid < PB) po[tid] = (double)prel[tid];
     for (int e = tid; e < 256; e += blockDim.x) {  // D^{-1} fragments
       const int f = e >> 5, lane = e & 31, mt = f >> 2, ks = f & 3;
-      po[e] = X[(mt * 8 + (lane >> 2)) * 17 + ks * 4 + (lane & 3)];
+      po[16 + e] = X[(mt * 8 + (lane >> 2)) * 17 + ks * 4 + (lane & 3)];
     }
+    __shared__ int s_mt;
+    if (tid == 0) s_mt = 0;
+    __syncthreads();
+    int mt_hi = 0;  // highest nonzero m-tile of T (+1) seen by this thread
     for (int e = tid; e < 16 * kwp; e += blockDim.x) {  // -(T D^{-1}) fragments
       const int f = e >> 5, lane = e & 31, mt = f >> 2, ks = f & 3;
       const int r = PB + mt * 8 + (lane >> 2), c = ks * 4 + (lane & 3);
       double acc = 0.0;
       for (int k = 0; k < PB; ++k) acc = fma(lt[r * PB + k], X[k * 17 + c], acc);
-      po[256 + e] = -acc;
+      po[PREC_HDR + e] = -acc;
+      if (lt[r * PB + c] != 0.0) mt_hi = max(mt_hi, mt + 1);  // T's own pattern decides
     }
-    if (tid < PB) po[256 + 16 * kwp + tid] = (double)prel[tid];
+    atomicMax(&s_mt, mt_hi);
+    __syncthreads();
+    if (tid == 0) mt_all[mtoff[blockIdx.x] + p] = (unsigned char)s_mt;
     __syncthreads();
   }
 }
@@ -165,6 +181,9 @@ struct PanelArgs {
   double* xs;
   long long xs_len;
   int nrhs, kwf, kwb, WR, stage_stride, ns;
+  const unsigned char* pmt;  // per panel: nonzero m-tiles of T; block s: forward at mtoff[s], backward after
+  const long long* mtoff;
+  int np_max;                // most panels of a block (shared-memory copy of the counts)
 };
 
 struct PanelSweep {
@@ -177,6 +196,7 @@ struct PanelSweep {
   uint64_t* empty;
   int n, kwp, WR, mtT;
   int* chunk;
+  const unsigned char* mt;   // this sweep's per-panel m-tile counts (shared memory)
 };
 
 template <bool FWD>
@@ -224,9 +244,10 @@ __device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& e
   const int stage = chunk % ns;
   mbar_wait(&S.full[stage], (chunk / ns) & 1);
   const double* rec = S.ring + (size_t)stage * S.a->stage_stride;
+  const int mtp = S.mt[p];  // nonzero m-tiles of this panel's T
   if (FWD) {  // the panel's row interchanges, moved to its front (every thread reads the same 16 pivots)
     bool any = false;
-    const double2* pv = reinterpret_cast<const double2*>(rec + 256 + 16 * kwp);
+    const double2* pv = reinterpret_cast<const double2*>(rec);
 #pragma unroll
     for (int t = 0; t < PB / 2; ++t) {
       const double2 v = pv[t];
@@ -235,7 +256,7 @@ __device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& e
     if (any) {
       if (warp == 0) {
         for (int t = 0; t < PB; ++t) {
-          const int p2 = __double2int_rn(rec[256 + 16 * kwp + t]);
+          const int p2 = __double2int_rn(rec[t]);
           if (p2 != t && lane < 16) {
             double* r1 = panel_row(S, base, t);
             double* r2 = panel_row(S, base, p2);
@@ -260,9 +281,9 @@ __device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& e
   // tiles: 0..3 = X = D^{-1} W (2 m x 2 n); 4.. = trailing rows += -(T D^{-1}) W.
   // Warp w takes tiles w, w+8, ... (all of the same n-tile, w & 1), at most
   // TG of them, k-steps interleaved across its tiles.
-  const int ntile = 4 + 2 * S.mtT;
+  const int ntile = 4 + 2 * mtp;
   constexpr int TG = 5;
-  const int nu = (ntile - warp + 7) >> 3;  // tiles of this warp (<= TG: ntile <= 40)
+  const int nu = warp < ntile ? (ntile - warp + 7) >> 3 : 0;  // tiles of this warp (<= TG: ntile <= 40)
   const double* bsel = (warp & 1) ? b1 : b0;
   double acc[TG][2];
   const double* ap[TG];
@@ -275,10 +296,10 @@ __device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& e
     ap[u] = rec + lane;
     if (u < nu) {
       if (t < 4) {
-        ap[u] = rec + (t >> 1) * 128 + lane;
+        ap[u] = rec + 16 + (t >> 1) * 128 + lane;
       } else {
         const int mt = (t - 4) >> 1;
-        ap[u] = rec + 256 + mt * 128 + lane;
+        ap[u] = rec + PREC_HDR + mt * 128 + lane;
         crow[u] = panel_row(S, base, PB + mt * 8 + g) + (t & 1) * 8 + 2 * q;
         const double2 c2 = *reinterpret_cast<const double2*>(crow[u]);
         acc[u][0] = c2.x;
@@ -318,8 +339,9 @@ template <bool FWD>
 __device__ __forceinline__ void panel_sweep(const PanelArgs& a, const LocalDesc& d, double* ring, uint64_t* full,
                                             uint64_t* empty, double* W, int& chunk) {
   const int tid = threadIdx.x;
+  const unsigned char* smt = reinterpret_cast<const unsigned char*>(W + (size_t)a.WR * PSR);
   PanelSweep S{&a, a.idx + d.idx_off, a.xs + d.idx_off, W, ring, full, empty, d.n, FWD ? a.kwf : a.kwb, a.WR, 0,
-               &chunk};
+               &chunk, smt + (FWD ? 0 : (d.n + PB - 1) / PB)};
   S.mtT = S.kwp >> 3;
   const int np = (S.n + PB - 1) / PB;
   // prologue: panel 0 and its trailing rows
@@ -361,11 +383,14 @@ __global__ void __launch_bounds__(PTHREADS, 2) k_local_panel(PanelArgs a) {
     }
     fence_mbar_init();
   }
-  __syncthreads();
   if (d.n == 0) return;
   const int np = (d.n + PB - 1) / PB;
+  // per-panel m-tile counts of both sweeps into shared memory (after the window)
+  unsigned char* smt = reinterpret_cast<unsigned char*>(sm + (size_t)ns * a.stage_stride + (size_t)a.WR * PSR);
+  for (int e = threadIdx.x; e < 2 * np; e += blockDim.x) smt[e] = a.pmt[a.mtoff[blockIdx.x] + e];
+  __syncthreads();
   if (threadIdx.x >= 256) {
-    if (threadIdx.x == 256) {  // producer: forward panels, then backward panels
+    if (threadIdx.x == 256) {  // producer: forward panels, then backward panels (used part only)
       const long long psf = panel_doubles(a.kwf), psb = panel_doubles(a.kwb);
       for (int c = 0; c < 2 * np; ++c) {
         const int stage = c % ns;
@@ -373,7 +398,7 @@ __global__ void __launch_bounds__(PTHREADS, 2) k_local_panel(PanelArgs a) {
         const bool f = c < np;
         const int pp = f ? c : c - np;
         const double* src = f ? a.pf + a.poff[2 * blockIdx.x] + pp * psf : a.pb + a.poff[2 * blockIdx.x + 1] + pp * psb;
-        const uint32_t bytes = (uint32_t)((f ? psf : psb) * 8);
+        const uint32_t bytes = (uint32_t)(panel_used(smt[c]) * 8);
         mbar_arrive_expect_tx(&full[stage], bytes);
         bulk_g2s(sm + (size_t)stage * a.stage_stride, src, bytes, &full[stage]);
       }
@@ -410,13 +435,14 @@ static int panel_stages(const HgPrecond* P) {
   const long long win = (long long)P->panel_wr * PSR * 8;
   static const int env = getenv("HG_PANEL_STAGES") ? atoi(getenv("HG_PANEL_STAGES")) : 0;
   if (env > 0) return std::min(env, PNS_MAX);
-  const long long budget = 113 * 1024 - 256;  // two CTAs per SM
+  const long long budget = 113 * 1024 - 256 - 2 * P->panel_np_max;  // two CTAs per SM
   return (int)std::max(3LL, std::min((long long)PNS_MAX, (budget - win) / ss));
 }
 
 static size_t panel_smem(const HgPrecond* P) {
   const long long ss = std::max(panel_doubles(P->panel_kwf), panel_doubles(P->panel_kwb));
-  return sizeof(double) * ((size_t)panel_stages(P) * ss + (size_t)P->panel_wr * PSR);
+  return sizeof(double) * ((size_t)panel_stages(P) * ss + (size_t)P->panel_wr * PSR) +
+         (size_t)((2 * P->panel_np_max + 15) / 16 * 16);
 }
 
 int launch_local_panel(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st) {
@@ -425,7 +451,8 @@ int launch_local_panel(HgPrecond* P, const double* R, long long ldr, int nrhs, c
   HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k_local_panel), smem, false));
   PanelArgs a{P->d_local, P->d_poff, P->d_local_idx, P->d_pfwd, P->d_pbwd, R, ldr, P->d_xsm, P->xs_len, nrhs,
               P->panel_kwf, P->panel_kwb, P->panel_wr,
-              (int)std::max(panel_doubles(P->panel_kwf), panel_doubles(P->panel_kwb)), panel_stages(P)};
+              (int)std::max(panel_doubles(P->panel_kwf), panel_doubles(P->panel_kwb)), panel_stages(P),
+              P->d_pmt, P->d_mtoff, P->panel_np_max};
   k_local_panel<<<P->n_local, PTHREADS, smem, st>>>(a);
   HG_LAUNCH_CHECK();
   return HG_OK;
@@ -459,14 +486,19 @@ int prepare_local_panel(HgPrecond* P) {
   P->panel_kwb = round8(kwb);
   P->panel_wr = 2 * PB + std::max(P->panel_kwf, P->panel_kwb);
   if (panel_smem(P) > 227 * 1024) return HG_OK;  // window too wide for shared memory: row kernel only
-  std::vector<long long> poff(2 * P->n_local);
-  long long pf = 0, pb = 0;
+  std::vector<long long> poff(2 * P->n_local), mtoff(P->n_local), mtoff_b(P->n_local);
+  long long pf = 0, pb = 0, pm = 0;
+  P->panel_np_max = 0;
   for (int s = 0; s < P->n_local; ++s) {
     const long long np = (P->h_local[s].n + PB - 1) / PB;
     poff[2 * s] = pf;
     poff[2 * s + 1] = pb;
+    mtoff[s] = pm;
+    mtoff_b[s] = pm + np;
+    pm += 2 * np;
     pf += np * panel_doubles(P->panel_kwf);
     pb += np * panel_doubles(P->panel_kwb);
+    P->panel_np_max = std::max(P->panel_np_max, (int)np);
   }
   HG_TRY(dev_upload(&P->d_poff, poff.data(), poff.size(), &P->device_bytes));
   // per-sweep offsets for the two conversion launches (temporaries)
@@ -480,17 +512,31 @@ int prepare_local_panel(HgPrecond* P) {
   HG_TRY(dev_upload(&d_pob, pob.data(), pob.size(), nullptr));
   HG_TRY(dev_upload<double>(&P->d_pfwd, nullptr, (size_t)pf, &P->device_bytes));
   HG_TRY(dev_upload<double>(&P->d_pbwd, nullptr, (size_t)pb, &P->device_bytes));
+  HG_TRY(dev_upload<unsigned char>(&P->d_pmt, nullptr, (size_t)pm, &P->device_bytes));
+  HG_TRY(dev_upload(&P->d_mtoff, mtoff.data(), mtoff.size(), &P->device_bytes));
+  long long* d_mtoff_b = nullptr;
+  HG_TRY(dev_upload(&d_mtoff_b, mtoff_b.data(), mtoff_b.size(), nullptr));
   const size_t cf = sizeof(double) * ((PB + P->panel_kwf) * PB + PB + PB * 17);
   const size_t cb = sizeof(double) * ((PB + P->panel_kwb) * PB + PB + PB * 17);
   HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k_panel_convert<true>), cf, false));
   HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k_panel_convert<false>), cb, false));
-  k_panel_convert<true><<<P->n_local, 128, cf>>>(P->d_local, P->d_fwd, d_pof, P->panel_kwf, P->d_pfwd);
+  k_panel_convert<true><<<P->n_local, 128, cf>>>(P->d_local, P->d_fwd, d_pof, P->panel_kwf, P->d_pfwd, P->d_mtoff,
+                                                   P->d_pmt);
   HG_LAUNCH_CHECK();
-  k_panel_convert<false><<<P->n_local, 128, cb>>>(P->d_local, P->d_bwd, d_pob, P->panel_kwb, P->d_pbwd);
+  k_panel_convert<false><<<P->n_local, 128, cb>>>(P->d_local, P->d_bwd, d_pob, P->panel_kwb, P->d_pbwd, d_mtoff_b,
+                                                    P->d_pmt);
   HG_LAUNCH_CHECK();
   HG_CUDA_TRY(cudaDeviceSynchronize());
   cudaFree(d_pof);
   cudaFree(d_pob);
+  cudaFree(d_mtoff_b);
+  {  // bytes one batched local solve streams (hg_precond_stat)
+    std::vector<unsigned char> mt((size_t)pm);
+    HG_CUDA_TRY(cudaMemcpy(mt.data(), P->d_pmt, mt.size(), cudaMemcpyDeviceToHost));
+    long long used = 0;
+    for (unsigned char v : mt) used += panel_used(v);
+    P->panel_stream_bytes = 8 * used;
+  }
 
   // guard: panel vs row solve on a seeded 16-column batch
   const int nr = HG_MAX_RHS;

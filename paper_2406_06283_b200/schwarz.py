@@ -543,13 +543,7 @@ class TwoLevelPreconditioner:
         self.panel_active = bool(lib.hg_precond_stat(h, _lib.STAT_PANEL_ACTIVE) == 1.0)
         self.panel_deviation = float(lib.hg_precond_stat(h, _lib.STAT_PANEL_DEVIATION))
         # factor bytes one batched local solve streams (16-row panel records, hg_local_panel.cu)
-        if self.panel_active and "local_kl" in arrays and len(arrays["local_kl"]):
-            r8 = lambda x: (int(x) + 7) // 8 * 8  # noqa: E731
-            kwf, kwb = r8(np.max(arrays["local_kl"])), r8(np.max(arrays["local_kv"]))
-            npan = sum((int(x) + 15) // 16 for x in arrays["local_n"])
-            self.panel_bytes = 8 * npan * ((256 + 16 * kwf + 16) + (256 + 16 * kwb + 16))
-        else:
-            self.panel_bytes = None
+        self.panel_bytes = int(lib.hg_precond_stat(h, _lib.STAT_PANEL_BYTES)) if self.panel_active else None
 
     # ------------------------------------------------------------------ API
     @property

@@ -15,7 +15,7 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "prof-512"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 P = hg.build_problem(cfg, cstab=None if cfg == "prof-512" else "cache", workers=int(os.environ.get("HG_WORKERS", "0")) or None)
 pre = hg.factorize(P.forms, P.dec, P.coarse)
-print("panel active", pre.panel_active, "deviation %.2e" % pre.panel_deviation)
+print("panel active", pre.panel_active, "deviation %.2e" % pre.panel_deviation, "bytes %.3f GB" % (pre.panel_bytes / 1e9))
 R = torch.from_numpy(np.random.default_rng(0).standard_normal((16, pre.n))).cuda()
 for _ in range(reps):
     pre.apply_multi(R)
