@@ -466,8 +466,10 @@ class TwoLevelPreconditioner:
             # dense mode: B0^{-1} applied as a streaming GEMV / DMMA GEMM beside the
             # local solves; kept only if it agrees with getrs (the reference's lu_solve)
             M["b0_dense_dev"] = None
-            # "1": every apply; "multi": batched applies only (the single apply keeps the chain)
-            dense = os.environ.get("HG_B0_DENSE", "0")
+            # "1": every apply; "multi" (default while B0^{-1} fits: m <= 20000, 3.2 GB): batched applies
+            # only — there the chain is the critical path, while the single apply keeps the chain
+            # (the 1.9 GB stream would contend with its local solves); "0": never
+            dense = os.environ.get("HG_B0_DENSE", "multi" if m <= 20000 else "0")
             if dense in ("1", "multi") or (dense == "auto" and m <= 20000):  # "auto": whenever it fits
                 torch = _torch()
                 B0 = np.ascontiguousarray(np.asarray(self._coarse.B0), dtype=np.float64)

@@ -212,10 +212,10 @@ def test_coarse_solve_modes_agree(name, monkeypatch):
     orc = OraclePreconditioner(P.forms, P.dec, P.coarse)
     R = np.random.default_rng(31).standard_normal((P.forms.n_dofs, 16))
     outs = {}
-    for dense in ("1", "0"):
+    for dense in ("1", "0", "multi"):
         monkeypatch.setenv("HG_B0_DENSE", dense)
         pre = hg.factorize(P.forms, P.dec, P.coarse)
-        assert pre.b0_dense == (dense == "1")
+        assert pre.b0_dense == (dense != "0")
         single = np.stack([pre.apply_coarse(R[:, c]) for c in (0, 9)], axis=1)
         outs[dense] = (pre.apply(R[:, 0]), pre.apply_multi(R), single)
         for k, c in enumerate((0, 9)):
@@ -224,6 +224,8 @@ def test_coarse_solve_modes_agree(name, monkeypatch):
         assert colrel(outs[dense][1], np.stack([pre.apply(R[:, c]) for c in range(16)], axis=1)) <= MULTI_RTOL
     assert rel(outs["1"][0], outs["0"][0]) <= 1e-12
     assert colrel(outs["1"][1], outs["0"][1]) <= 1e-12
+    assert np.array_equal(outs["multi"][0], outs["0"][0])  # "multi": the single apply keeps the chain
+    assert np.array_equal(outs["multi"][1], outs["1"][1])  # and the batched one uses B0^{-1}
 
 
 def _fov_reference_loop(forms, apply_T, mode, samples=0, rng=None):

@@ -47,6 +47,7 @@ def test_lost_zt_times_out_and_poisons(cfg1, short_spin, monkeypatch, mode, batc
     hung GPU."""
     P, g, coarse = cfg1
     monkeypatch.setenv("HG_B0_MODE", mode)
+    monkeypatch.setenv("HG_B0_DENSE", "0")  # the chain kernels (the ones that wait on Z^T r)
     pre = hg.factorize(P.forms, P.dec, coarse)
     assert pre.b0_mode == int(mode)
     R = np.stack([g["r"], g["u"]], axis=1)
