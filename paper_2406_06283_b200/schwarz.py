@@ -469,7 +469,8 @@ class TwoLevelPreconditioner:
             # "1": every apply; "multi" (default while B0^{-1} fits: m <= 20000, 3.2 GB): batched applies
             # only — there the chain is the critical path, while the single apply keeps the chain
             # (the 1.9 GB stream would contend with its local solves); "0": never
-            dense = os.environ.get("HG_B0_DENSE", "multi" if m <= 20000 else "0")
+            host_only = getattr(self, "_host_only", False)  # host_image(): no device to invert on
+            dense = os.environ.get("HG_B0_DENSE", "multi" if m <= 20000 and not host_only else "0")
             if dense in ("1", "multi") or (dense == "auto" and m <= 20000):  # "auto": whenever it fits
                 torch = _torch()
                 B0 = np.ascontiguousarray(np.asarray(self._coarse.B0), dtype=np.float64)
