@@ -194,6 +194,22 @@ int hg_device_sync(void);
  * finalizers run; the Python binding registers this with atexit). */
 int hg_shutdown(void);
 
+/* ---- setup on the device ---- */
+/* Coarse operator: B0 = 0.5 (Z^T B Z + (Z^T B Z)^T) (eigencoarse.py:286-287)
+ * from the desc's global CSR of B and its Z blocks (n, nnz, indptr, indices,
+ * b_data, m, n_cblk, cblk_*, z_len, z_data; nothing else is read), with the
+ * block interaction lists pair_ptr[n_cblk+1] / pair_blk (blocks a whose
+ * dofs couple to block b through B, for b in order); then its LU with partial
+ * pivoting (LAPACK getrf semantics, schwarz.py:90: 64-column panels, row
+ * interchanges over whole rows, multipliers by the reciprocal pivot) and the
+ * rank certificate of coarse._sym_extreme_certificate: cert_out[0] =
+ * |lambda|_max estimate (power iteration on B0), cert_out[1] = ||B0^{-1}||
+ * estimate (inverse iteration through the LU), cert_iters steps each.  Any
+ * host output may be NULL: b0_out, lu_out (m*m row-major), piv_out (m,
+ * 0-based), info_out (getrf INFO), cert_out (2). */
+int hg_coarse_setup(const HgPrecondDesc* desc, const int32_t* pair_ptr, const int32_t* pair_blk, double* b0_out,
+                    double* lu_out, int32_t* piv_out, int32_t* info_out, double* cert_out, int32_t cert_iters);
+
 /* ---- preconditioner (schwarz.factorize / TwoLevelPreconditioner) ---- */
 int hg_precond_create(const HgPrecondDesc* desc, HgPrecond** out);
 /* Fault state of a handle (no synchronisation).  The coarse solve is

@@ -128,6 +128,10 @@ SIGNATURES = {
     "hg_debug_set": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int64]),
     "hg_precond_read": (ctypes.c_int, [_vp, ctypes.c_int32, _f64p, ctypes.c_int64]),
     "hg_precond_stat": (ctypes.c_double, [_vp, ctypes.c_int32]),
+    "hg_coarse_setup": (
+        ctypes.c_int,
+        [ctypes.POINTER(HgPrecondDesc), _i32p, _i32p, _f64p, _f64p, _i32p, _i32p, _f64p, ctypes.c_int32],
+    ),
 }
 STAT_PANEL_ACTIVE, STAT_PANEL_DEVIATION, STAT_PANEL_BYTES = 1, 2, 3
 FIELD_LOCAL_FWD, FIELD_LOCAL_BWD = 1, 2

@@ -26,6 +26,7 @@ scalable variants SURVEY §8c asks for on the ~1M-dof configs:
   if the certificate cannot rule out near-null columns is the dense eigh run.
 """
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -401,8 +402,76 @@ def _near_null_columns(mat):
     return drop
 
 
-def build_coarse_space(results, selection, dec, forms, dense_rank_filter_max=3000):
-    """Z blocks and B0 = Z^T B Z, symmetrised and rank filtered (eigencoarse.py:248-321)."""
+def device_available():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def coarse_operator_device(forms, blocks, pairs, certificate_iters=60):
+    """B0 = 0.5 (Z^T B Z + (Z^T B Z)^T), its getrf factors and the rank
+    certificate's two estimates, computed on the device (hg_coarse_setup,
+    csrc/hg_coarse_setup.cu; eigencoarse.py:286-287, schwarz.py:90).
+    Returns (B0, (lu, piv), info, (lambda_max, ||B0^-1||))."""
+    import ctypes
+
+    from . import _lib
+
+    B = sp.csr_matrix(forms.helmholtz)
+    B.sort_indices()
+    n = B.shape[0]
+    nb = len(blocks)
+    m = sum(b.shape[1] for _, b in blocks)
+    keep = []
+
+    def arr(a, dtype, ctype):
+        a = np.ascontiguousarray(a, dtype=dtype)
+        keep.append(a)
+        return _lib.ptr(a, ctype)
+
+    i32, i64, f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    d = _lib.HgPrecondDesc()
+    d.n, d.nnz = n, B.nnz
+    d.indptr = arr(B.indptr, np.int32, i32)
+    d.indices = arr(B.indices, np.int32, i32)
+    d.b_data = arr(B.data, np.float64, f64)
+    d.m, d.n_cblk = m, nb
+    d.cblk_n = arr([i.size for i, _ in blocks], np.int32, i32)
+    d.cblk_m = arr([b.shape[1] for _, b in blocks], np.int32, i32)
+    d.cblk_idx_off = arr(np.concatenate([[0], np.cumsum([i.size for i, _ in blocks])]), np.int64, i64)
+    d.cblk_idx = arr(np.concatenate([i for i, _ in blocks]), np.int32, i32)
+    d.cblk_z_off = arr(np.concatenate([[0], np.cumsum([b.size for _, b in blocks])[:-1]]), np.int64, i64)
+    z = np.concatenate([b.ravel() for _, b in blocks])
+    d.z_len = z.size
+    d.z_data = arr(z, np.float64, f64)
+    nbr = [[] for _ in range(nb)]
+    for a, b in pairs:
+        if blocks[a][1].shape[1] and blocks[b][1].shape[1]:
+            nbr[b].append(a)
+    pair_ptr = np.concatenate([[0], np.cumsum([len(x) for x in nbr])]).astype(np.int32)
+    pair_blk = np.asarray([a for x in nbr for a in x] or [0], dtype=np.int32)
+    B0 = np.empty((m, m))
+    lu = np.empty((m, m))
+    piv = np.empty(m, dtype=np.int32)
+    info = np.zeros(1, dtype=np.int32)
+    cert = np.zeros(2)
+    _lib.check(_lib.load().hg_coarse_setup(ctypes.byref(d), _lib.ptr(pair_ptr, i32), _lib.ptr(pair_blk, i32),
+                                           _lib.ptr(B0, f64), _lib.ptr(lu, f64), _lib.ptr(piv, i32),
+                                           _lib.ptr(info, i32), _lib.ptr(cert, f64), int(certificate_iters)),
+               "hg_coarse_setup")
+    return B0, (lu, piv.astype(np.int64)), int(info[0]), (float(cert[0]), float(cert[1]))
+
+
+def build_coarse_space(results, selection, dec, forms, dense_rank_filter_max=3000, device=None):
+    """Z blocks and B0 = Z^T B Z, symmetrised and rank filtered (eigencoarse.py:248-321).
+
+    ``device``: build B0, its LU and the rank certificate on the GPU
+    (coarse_operator_device); None = when a CUDA device is present and the
+    coarse space is large (m > dense_rank_filter_max), HG_HOST_SETUP=1 forces
+    the host."""
     n = forms.n_dofs
     blocks, meta = [], []
     for res, m, sub in zip(results, selection.m_per_subdomain, dec.coarse):
@@ -417,23 +486,33 @@ def build_coarse_space(results, selection, dec, forms, dense_rank_filter_max=300
         return CoarseSpace(blocks, n, counts, selection.tau, selection.theta, np.zeros((0, 0)), [], [])
 
     offs = np.concatenate([[0], np.cumsum(counts)])
-    B0 = np.zeros((m_total, m_total))
-    B = forms.helmholtz
-    for a, b in _interaction_pairs(forms, [idx for idx, _ in blocks]):
-        if counts[a] == 0 or counts[b] == 0:
-            continue
-        ia, za = blocks[a]
-        ib, zb = blocks[b]
-        Bab = submatrix(B, ia, ib)
-        B0[offs[a]:offs[a + 1], offs[b]:offs[b + 1]] = za.T @ (Bab @ zb)
-    B0 = 0.5 * (B0 + B0.T)
-
+    pairs = _interaction_pairs(forms, [idx for idx, _ in blocks])
+    if device is None:
+        device = (m_total > dense_rank_filter_max and device_available()
+                  and os.environ.get("HG_HOST_SETUP", "0") != "1")
     keep = list(range(m_total))
     removed = []
     certified = False
     b0_lu = None
-    if m_total > dense_rank_filter_max:
-        certified, b0_lu = _sym_extreme_certificate(B0, _PIVOT_RTOL)
+    if device:
+        B0, lu_piv, info, (lmax, inv_max) = coarse_operator_device(forms, blocks, pairs)
+        if info == 0:
+            b0_lu = lu_piv
+            if m_total > dense_rank_filter_max:  # coarse._sym_extreme_certificate's test
+                certified = (1.0 / inv_max) > 1e6 * _PIVOT_RTOL * lmax
+    else:
+        B0 = np.zeros((m_total, m_total))
+        B = forms.helmholtz
+        for a, b in pairs:
+            if counts[a] == 0 or counts[b] == 0:
+                continue
+            ia, za = blocks[a]
+            ib, zb = blocks[b]
+            Bab = submatrix(B, ia, ib)
+            B0[offs[a]:offs[a + 1], offs[b]:offs[b + 1]] = za.T @ (Bab @ zb)
+        B0 = 0.5 * (B0 + B0.T)
+        if m_total > dense_rank_filter_max:
+            certified, b0_lu = _sym_extreme_certificate(B0, _PIVOT_RTOL)
     if not certified:
         while keep:
             drop = _near_null_columns(B0[np.ix_(keep, keep)])

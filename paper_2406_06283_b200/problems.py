@@ -216,6 +216,10 @@ def solve_local_gevps(forms, dec, method="auto", n_wanted=None, workers=None):
     small (<= 2000 active dofs), Lanczos otherwise.  Runs in a fork pool."""
     if method == "auto":
         method = "dense" if max(s.ovdof.size for s in dec.coarse) <= 2000 else "lanczos"
+    if method == "device":  # every subdomain at once on the GPU (gevp_device.py, SURVEY §8f item 3)
+        from .gevp_device import solve_local_gevps_device
+
+        return solve_local_gevps_device(forms, dec, n_wanted)
     _G["args"] = (forms, dec, method, n_wanted)
     idx = list(range(dec.n_coarse))
     workers = workers or min(len(idx), os.cpu_count() or 1)
