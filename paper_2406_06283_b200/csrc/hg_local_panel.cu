@@ -283,49 +283,52 @@ __device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& e
   // TG of them, k-steps interleaved across its tiles.
   const int ntile = 4 + 2 * mtp;
   constexpr int TG = 5;
-  const int nu = warp < ntile ? (ntile - warp + 7) >> 3 : 0;  // tiles of this warp (<= TG: ntile <= 40)
   const double* bsel = (warp & 1) ? b1 : b0;
-  double acc[TG][2];
-  const double* ap[TG];
-  double* crow[TG];
+  // groups of TG tiles per warp (one group while ntile <= 40, i.e. kw <= 144)
+  for (int t0 = warp; t0 < ntile; t0 += 8 * TG) {
+    const int nu = min(TG, (ntile - t0 + 7) >> 3);  // tiles of this warp in this group
+    double acc[TG][2];
+    const double* ap[TG];
+    double* crow[TG];
 #pragma unroll
-  for (int u = 0; u < TG; ++u) {
-    const int t = warp + 8 * u;
-    acc[u][0] = acc[u][1] = 0.0;
-    crow[u] = nullptr;
-    ap[u] = rec + lane;
-    if (u < nu) {
-      if (t < 4) {
-        ap[u] = rec + 16 + (t >> 1) * 128 + lane;
-      } else {
-        const int mt = (t - 4) >> 1;
-        ap[u] = rec + PREC_HDR + mt * 128 + lane;
-        crow[u] = panel_row(S, base, PB + mt * 8 + g) + (t & 1) * 8 + 2 * q;
-        const double2 c2 = *reinterpret_cast<const double2*>(crow[u]);
-        acc[u][0] = c2.x;
-        acc[u][1] = c2.y;
+    for (int u = 0; u < TG; ++u) {
+      const int t = t0 + 8 * u;
+      acc[u][0] = acc[u][1] = 0.0;
+      crow[u] = nullptr;
+      ap[u] = rec + lane;
+      if (u < nu) {
+        if (t < 4) {
+          ap[u] = rec + 16 + (t >> 1) * 128 + lane;
+        } else {
+          const int mt = (t - 4) >> 1;
+          ap[u] = rec + PREC_HDR + mt * 128 + lane;
+          crow[u] = panel_row(S, base, PB + mt * 8 + g) + (t & 1) * 8 + 2 * q;
+          const double2 c2 = *reinterpret_cast<const double2*>(crow[u]);
+          acc[u][0] = c2.x;
+          acc[u][1] = c2.y;
+        }
       }
     }
-  }
 #pragma unroll
-  for (int ks = 0; ks < 4; ++ks) {
+    for (int ks = 0; ks < 4; ++ks) {
 #pragma unroll
-    for (int u = 0; u < TG; ++u)
-      if (u < nu) dmma_p(acc[u], ap[u][ks * 32], bsel[ks]);
-  }
+      for (int u = 0; u < TG; ++u)
+        if (u < nu) dmma_p(acc[u], ap[u][ks * 32], bsel[ks]);
+    }
 #pragma unroll
-  for (int u = 0; u < TG; ++u) {
-    if (u >= nu) continue;
-    const int t = warp + 8 * u;
-    if (t < 4) {
-      const int r = (t >> 1) * 8 + g, c = (t & 1) * 8 + 2 * q;
-      double* xs = S.xs + (FWD ? (long long)(j0 + r) : (long long)(S.n - 1 - (j0 + r)));
-      if (j0 + r < S.n) {
-        if (c < S.a->nrhs) xs[(long long)c * S.a->xs_len] = acc[u][0];
-        if (c + 1 < S.a->nrhs) xs[(long long)(c + 1) * S.a->xs_len] = acc[u][1];
+    for (int u = 0; u < TG; ++u) {
+      if (u >= nu) continue;
+      const int t = t0 + 8 * u;
+      if (t < 4) {
+        const int r = (t >> 1) * 8 + g, c = (t & 1) * 8 + 2 * q;
+        double* xs = S.xs + (FWD ? (long long)(j0 + r) : (long long)(S.n - 1 - (j0 + r)));
+        if (j0 + r < S.n) {
+          if (c < S.a->nrhs) xs[(long long)c * S.a->xs_len] = acc[u][0];
+          if (c + 1 < S.a->nrhs) xs[(long long)(c + 1) * S.a->xs_len] = acc[u][1];
+        }
+      } else {
+        *reinterpret_cast<double2*>(crow[u]) = make_double2(acc[u][0], acc[u][1]);
       }
-    } else {
-      *reinterpret_cast<double2*>(crow[u]) = make_double2(acc[u][0], acc[u][1]);
     }
   }
   // entering rows take the slots of the previous panel (finished)
