@@ -609,12 +609,17 @@ static int precond_apply_multi_core_impl(HgPrecond* P, const double* R, long lon
   }
   HG_TRY(multi_prepare(P));
   if (P->m > 0 && P->d_b0_inv) {
-    HG_TRY(launch_zt_multi(P, R, ldr, nrhs, st));
+    // dense coarse: no kernel waits on another, so the long local solve is
+    // issued FIRST and takes its SMs; Z^T R -> B0^{-1} -> Z Y fill the rest
     HG_CUDA_TRY(cudaEventRecord(P->ev_fork, st));
     HG_CUDA_TRY(cudaStreamWaitEvent(P->aux, P->ev_fork, 0));
+    HG_TRY(launch_local_batch(P, R, ldr, nrhs, st));
+    HG_TRY(launch_zt_multi(P, R, ldr, nrhs, P->aux));
     HG_TRY(launch_b0_dense_multi(P, nrhs, P->aux));
     HG_TRY(launch_zy_multi(P, nrhs, P->aux));
     HG_CUDA_TRY(cudaEventRecord(P->ev_join, P->aux));
+    HG_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_join, 0));
+    return launch_assemble_multi(P, true, true, OUT, ldo, nrhs, st);
   } else if (P->m > 0) {
     HG_CUDA_TRY(cudaEventRecord(P->ev_fork, st));
     HG_CUDA_TRY(cudaStreamWaitEvent(P->aux, P->ev_fork, 0));

@@ -46,7 +46,7 @@ def _torch():
     return torch
 
 
-def solve_local_gevps_device(forms, dec, n_wanted, shift=2.0, tol=1e-13, max_restarts=60, seed=7919,
+def solve_local_gevps_device(forms, dec, n_wanted, shift=2.0, tol=1e-15, max_restarts=200, seed=7919,
                              keep_extra=20, verbose=False):
     """[LocalGevpResult] for every coarse subdomain (partial spectra: the
     lowest ``n_wanted + 1`` finite eigenvalues), as coarse.solve_gevp_lanczos
