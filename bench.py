@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--cstab", default="cache", help="'cache' (recorded setup constant), 'auto' (recompute)")
     ap.add_argument("--orth", default="dcgs2", choices=["dcgs2", "measured"])
     ap.add_argument("--single-steps", type=int, default=3, help="one-at-a-time solves timed for single_rhs")
+    ap.add_argument("--gevp", default="auto", choices=["auto", "device"],
+                    help="local GEVPs: host ARPACK restatement (auto) or the batched device Lanczos")
     return ap.parse_args()
 
 
@@ -262,12 +264,12 @@ def build_shared(args, dist):
     import paper_2406_06283_b200 as hg
 
     if dist.world == 1:
-        return hg.build_problem(args.config, cstab=args.cstab, verbose=True)
+        return hg.build_problem(args.config, cstab=args.cstab, verbose=True, gevp=args.gevp)
     path = os.path.join(tempfile.gettempdir(), "hg_setup_%s_%s_%s.pkl" % (
         args.config, os.environ.get("MASTER_PORT", "0"), os.environ.get("TORCHELASTIC_RUN_ID", "run")))
     P, ok = None, 0.0
     if dist.rank == 0:
-        P = hg.build_problem(args.config, cstab=args.cstab, verbose=True)
+        P = hg.build_problem(args.config, cstab=args.cstab, verbose=True, gevp=args.gevp)
         try:
             with open(path + ".tmp", "wb") as fh:
                 pickle.dump(P, fh, protocol=pickle.HIGHEST_PROTOCOL)
@@ -308,6 +310,10 @@ def run_ours(args, dist):
     t_fact = time.perf_counter() - t0
     setup = dict(P.times)
     setup["factorize_upload"] = t_fact
+    setup.update({"factorize." + k: v for k, v in getattr(pre, "setup_times", {}).items()})
+    cb = getattr(P.coarse, "build_seconds", None) if P.coarse is not None else None
+    if cb:
+        setup.update({"coarse." + k: v for k, v in cb.items() if k != "device"})
     log("setup %.1f s + factorize/upload %.1f s; device bytes %.2f GB" % (t_setup, t_fact, pre.device_bytes / 1e9))
 
     rhs_host = P.rhs if P.rhs.ndim == 2 else P.rhs[:, None]
@@ -514,6 +520,9 @@ def run_ours(args, dist):
         "solve_roofline": solve_roof,
         "roofline": roofline,
         "setup_s": {k: round(v, 2) for k, v in setup.items()},
+        "setup_device": {"local_factor": bool(getattr(pre, "device_factor", False)),
+                         "coarse_operator": bool(cb and cb.get("device")),
+                         "gevp": args.gevp},
         "gpu_launches": launches,
         "clocks": clk,
     }

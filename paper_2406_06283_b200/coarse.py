@@ -494,6 +494,9 @@ def build_coarse_space(results, selection, dec, forms, dense_rank_filter_max=300
     removed = []
     certified = False
     b0_lu = None
+    import time
+
+    t0 = time.perf_counter()
     if device:
         B0, lu_piv, info, (lmax, inv_max) = coarse_operator_device(forms, blocks, pairs)
         if info == 0:
@@ -536,6 +539,8 @@ def build_coarse_space(results, selection, dec, forms, dense_rank_filter_max=300
         meta = [meta[i] for i in keep]
         counts = [b.shape[1] for _, b in blocks]
     cs = CoarseSpace(blocks, n, counts, selection.tau, selection.theta, B0, meta, removed)
+    cs.build_seconds = {"operator_lu_certificate" if device else "operator_certificate": time.perf_counter() - t0,
+                        "device": bool(device)}
     if b0_lu is not None and not removed:
         cs._b0_lu = b0_lu  # getrf of B0 already computed by the certificate; factorize reuses it
     return cs

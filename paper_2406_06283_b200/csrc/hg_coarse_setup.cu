@@ -270,16 +270,9 @@ __global__ void __launch_bounds__(256) k_lu_solve_block(const double* __restrict
   if (threadIdx.x < rb) x[r0 + threadIdx.x] = xb[threadIdx.x];
 }
 
-__global__ void k_apply_perm(const int* __restrict__ piv, int m, double* __restrict__ x) {
-  if (blockIdx.x == 0 && threadIdx.x == 0)
-    for (int i = 0; i < m; ++i) {
-      const int p = piv[i];
-      if (p != i) {
-        const double t = x[i];
-        x[i] = x[p];
-        x[p] = t;
-      }
-    }
+__global__ void k_gather(const int* __restrict__ perm, int m, const double* __restrict__ x, double* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) y[i] = x[perm[i]];
 }
 
 }  // namespace hg
@@ -314,9 +307,28 @@ double host_norm(const std::vector<double>& v) {
 }
 }  // namespace
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
+namespace {
+struct PhaseClock {  // HG_SETUP_TIMING=1: seconds per phase on stderr
+  bool on = getenv("HG_SETUP_TIMING") && getenv("HG_SETUP_TIMING")[0] == '1';
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void tick(const char* what) {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[hg_coarse_setup] %-12s %.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    t = now;
+  }
+};
+}  // namespace
+
 extern "C" int hg_coarse_setup(const HgPrecondDesc* D, const int32_t* pair_ptr, const int32_t* pair_blk,
                                double* b0_out, double* lu_out, int32_t* piv_out, int32_t* info_out,
                                double* cert_out, int32_t cert_iters) {
+  PhaseClock clk;
   if (!D || D->m <= 0 || !D->indptr || !D->z_data || !pair_ptr || !pair_blk) {
     set_error("hg_coarse_setup: bad argument");
     return HG_ERR_ARG;
@@ -378,7 +390,9 @@ extern "C" int hg_coarse_setup(const HgPrecondDesc* D, const int32_t* pair_ptr, 
   const long long mm = (long long)m * m;
   k_symmetrise<<<ceil_div(mm, 256), 256, 0, st>>>(d_B0, m);
   HG_LAUNCH_CHECK();
+  clk.tick("B0");
   if (b0_out) HG_CUDA_TRY(cudaMemcpy(b0_out, d_B0, sizeof(double) * mm, cudaMemcpyDeviceToHost));
+  clk.tick("B0 to host");
   if (!lu_out && !piv_out && !cert_out) return HG_OK;
 
   // ---- getrf in a copy (B0 is kept for the certificate's power iteration)
@@ -407,11 +421,13 @@ extern "C" int hg_coarse_setup(const HgPrecondDesc* D, const int32_t* pair_ptr, 
     }
   }
   HG_CUDA_TRY(cudaDeviceSynchronize());
+  clk.tick("getrf");
   int info = 0;
   HG_CUDA_TRY(cudaMemcpy(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost));
   if (info_out) *info_out = info;
   if (lu_out) HG_CUDA_TRY(cudaMemcpy(lu_out, d_LU, sizeof(double) * mm, cudaMemcpyDeviceToHost));
   if (piv_out) HG_CUDA_TRY(cudaMemcpy(piv_out, d_piv, sizeof(int) * m, cudaMemcpyDeviceToHost));
+  clk.tick("LU to host");
 
   // ---- certificate (coarse._sym_extreme_certificate): power iteration on B0
   // for |lambda|_max, inverse iteration through the LU for 1 / |lambda|_min
@@ -438,12 +454,20 @@ extern "C" int hg_coarse_setup(const HgPrecondDesc* D, const int32_t* pair_ptr, 
       lmax = ny / nx;
       for (int i = 0; i < m; ++i) hx[i] = hy[i] / ny;
     }
+    clk.tick("power iter");
+    std::vector<int> hpiv(m), perm(m);
+    HG_CUDA_TRY(cudaMemcpy(hpiv.data(), d_piv, sizeof(int) * m, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < m; ++i) perm[i] = i;
+    for (int i = 0; i < m; ++i)
+      if (hpiv[i] != i) std::swap(perm[i], perm[hpiv[i]]);  // (P b)[i] = b[perm[i]] (getrs row interchanges)
+    int* d_perm = nullptr;
+    HG_TRY(B.add(&d_perm, perm.data(), (size_t)m));
     for (double& v : hx) v = rnd();
     const int K = ceil_div(m, CS_NB);
     for (int it = 0; it < iters; ++it) {
       const double nx = host_norm(hx);
-      HG_CUDA_TRY(cudaMemcpy(d_y, hx.data(), sizeof(double) * m, cudaMemcpyHostToDevice));
-      k_apply_perm<<<1, 1, 0, st>>>(d_piv, m, d_y);  // getrs: row interchanges first
+      HG_CUDA_TRY(cudaMemcpy(d_x, hx.data(), sizeof(double) * m, cudaMemcpyHostToDevice));
+      k_gather<<<ceil_div(m, 256), 256, 0, st>>>(d_perm, m, d_x, d_y);  // getrs: row interchanges first
       for (int t = 0; t < K; ++t) k_lu_solve_block<<<1, 256, 0, st>>>(d_LU, m, t, false, d_y);
       for (int t = K - 1; t >= 0; --t) k_lu_solve_block<<<1, 256, 0, st>>>(d_LU, m, t, true, d_y);
       HG_LAUNCH_CHECK();
@@ -454,6 +478,7 @@ extern "C" int hg_coarse_setup(const HgPrecondDesc* D, const int32_t* pair_ptr, 
     }
     cert_out[0] = lmax;
     cert_out[1] = inv_max;
+    clk.tick("inverse iter");
   }
   return HG_OK;
 }

@@ -220,6 +220,10 @@ class TwoLevelPreconditioner:
     """Device-resident M^{-1} r = Z B0^{-1} Z^T r + sum_s E_s B_s^{-1} R_s r."""
 
     def __init__(self, forms, dec, coarse=None, b0_lu=None, keep_image=False):
+        import time
+
+        self._t = time.perf_counter
+        self.setup_times = {}
         self._keep_image = keep_image
         self._image_arrays = None
         self.forms = forms
@@ -241,6 +245,7 @@ class TwoLevelPreconditioner:
         # ---- local factorisations (schwarz.py:83-85, 104-131): on the device
         # (hg_factor.cu, dgbtrf semantics) unless a block's band is wider than
         # the compiled windows or HG_HOST_FACTOR=1 asks for LAPACK dgbtrf here
+        t0 = self._t()
         self.local_solvers = []
         factors = []
         blocks = []
@@ -262,6 +267,7 @@ class TwoLevelPreconditioner:
             else:
                 f = band_lu(sp.csr_matrix((0, 0)))
             factors.append((ls.idof, f))
+        self.setup_times["local_blocks"] = self._t() - t0
 
         # ---- coarse operator (schwarz.py:87-100)
         cblocks = []
@@ -288,7 +294,9 @@ class TwoLevelPreconditioner:
         if getattr(self, "_host_only", False):
             self._image_arrays, self._meta = arrays, meta
             return
-        self._create(arrays, meta)
+        t0 = self._t()
+        self._create(arrays, meta)  # upload + device band LU + panel records
+        self.setup_times["create"] = self._t() - t0
         if "factor_info" in arrays:
             self._check_device_factor(arrays, meta)
             if self._keep_image:  # the cache stores the device-built records, not the factor inputs
@@ -439,6 +447,7 @@ class TwoLevelPreconditioner:
         M["b0_dense"] = False
         if m:
             P = int(os.environ.get("HG_B0_PANEL", "64"))
+            t0 = self._t()
             T = pack_b0_tiles(lu, piv, P)
             # coarse-solve kernel: one DSMEM cluster when the x ring fits in shared memory
             cs = min(16, T.K)
@@ -450,6 +459,8 @@ class TwoLevelPreconditioner:
                 T = T.premultiply()  # tiles D_t^{-1} T[t, j]: rows of a panel finish independently
             # guard: the tiled algorithm (inverted diagonal blocks) must agree with getrs on several
             # vectors (a getrs-equivalent operator: explicit inverses of 64x64 blocks)
+            self.setup_times["b0_tiles"] = self._t() - t0
+            t0 = self._t()
             rng = np.random.default_rng(0)
             dev = 0.0
             for _ in range(4):
@@ -461,6 +472,8 @@ class TwoLevelPreconditioner:
                     "coarse tile factorisation deviates from getrs by %.2e (B0 too ill-conditioned for "
                     "inverted %dx%d diagonal blocks)" % (dev, P, P))
             self.b0_tiles = T
+            self.setup_times["b0_guard"] = self._t() - t0
+            t0 = self._t()
             M["b0_tile_dev"] = dev
             M["b0_bytes"] = int(T.nbytes + 4 * m + 4 * T.tile_col.size)
             # dense mode: B0^{-1} applied as a streaming GEMV / DMMA GEMM beside the
@@ -490,6 +503,7 @@ class TwoLevelPreconditioner:
                     M["b0_bytes_multi"] = int(8 * m * m + 16 * m)
                     if dense != "multi":
                         M["b0_bytes"] = int(8 * m * m + 16 * m)
+            self.setup_times["b0_inverse"] = self._t() - t0
             M["n_cblk"] = len(cblocks)
             put("cblk_n", [i.size for i, _ in cblocks], i32)
             put("cblk_m", [b.shape[1] for _, b in cblocks], i32)

@@ -39,11 +39,22 @@ def test_device_gevp_matches_host_lanczos(name):
     assert worst <= 1e-10, worst
 
 
-def test_preconditioner_from_device_gevps():
-    P_host = hg.build_problem("3", cstab="cache")
-    P_dev = hg.build_problem("3", cstab="cache", gevp="device")
-    assert P_dev.selection.m_per_subdomain == P_host.selection.m_per_subdomain
-    pre_h = hg.factorize(P_host.forms, P_host.dec, P_host.coarse)
-    pre_d = hg.factorize(P_dev.forms, P_dev.dec, P_dev.coarse)
-    r = np.random.default_rng(8).standard_normal(pre_h.n)
-    assert rel(pre_d.apply(r), pre_h.apply(r)) <= 1e-10
+@pytest.mark.parametrize("name", ["3", "2"])
+def test_preconditioner_from_device_gevps(name):
+    """Against the host Lanczos restatement (same shifted operator) the
+    preconditioners agree to 1e-10.  Against the reference's dense path
+    (gamma = 2 k^2 squeezes the finite spectrum into a relative width of
+    ~1e-3, so its eigenvectors are the less accurate ones) they agree to
+    1e-9."""
+    P_lz = hg.build_problem(name, cstab="cache", gevp="lanczos")
+    P_dev = hg.build_problem(name, cstab="cache", gevp="device")
+    P_dense = hg.build_problem(name, cstab="cache", gevp="dense")
+    assert P_dev.selection.m_per_subdomain == P_lz.selection.m_per_subdomain == P_dense.selection.m_per_subdomain
+    r = np.random.default_rng(8).standard_normal(P_lz.forms.n_dofs)
+    y_lz = hg.factorize(P_lz.forms, P_lz.dec, P_lz.coarse).apply(r)
+    y_dev = hg.factorize(P_dev.forms, P_dev.dec, P_dev.coarse).apply(r)
+    y_dense = hg.factorize(P_dense.forms, P_dense.dec, P_dense.coarse).apply(r)
+    print("%s: device vs host Lanczos %.2e, device vs dense %.2e, host Lanczos vs dense %.2e"
+          % (name, rel(y_dev, y_lz), rel(y_dev, y_dense), rel(y_lz, y_dense)))
+    assert rel(y_dev, y_lz) <= 1e-10
+    assert rel(y_dev, y_dense) <= 1e-9
