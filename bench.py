@@ -264,12 +264,12 @@ def build_shared(args, dist):
     import paper_2406_06283_b200 as hg
 
     if dist.world == 1:
-        return hg.build_problem(args.config, cstab=args.cstab, verbose=True, gevp=args.gevp)
+        return hg.build_problem(args.config, cstab=args.cstab, verbose=True, gevp=getattr(args, "gevp", "auto"))
     path = os.path.join(tempfile.gettempdir(), "hg_setup_%s_%s_%s.pkl" % (
         args.config, os.environ.get("MASTER_PORT", "0"), os.environ.get("TORCHELASTIC_RUN_ID", "run")))
     P, ok = None, 0.0
     if dist.rank == 0:
-        P = hg.build_problem(args.config, cstab=args.cstab, verbose=True, gevp=args.gevp)
+        P = hg.build_problem(args.config, cstab=args.cstab, verbose=True, gevp=getattr(args, "gevp", "auto"))
         try:
             with open(path + ".tmp", "wb") as fh:
                 pickle.dump(P, fh, protocol=pickle.HIGHEST_PROTOCOL)
@@ -522,7 +522,7 @@ def run_ours(args, dist):
         "setup_s": {k: round(v, 2) for k, v in setup.items()},
         "setup_device": {"local_factor": bool(getattr(pre, "device_factor", False)),
                          "coarse_operator": bool(cb and cb.get("device")),
-                         "gevp": args.gevp},
+                         "gevp": getattr(args, "gevp", "auto")},
         "gpu_launches": launches,
         "clocks": clk,
     }

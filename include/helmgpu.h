@@ -149,7 +149,8 @@ typedef struct {
   int32_t b0_mode;
   int32_t b0_cluster;
   int32_t b0_ring;
-  /* Optional dense B0^{-1} (m x m, row-major; NULL = none).  When given, the
+  /* Optional dense B0^{-1} (m x m, row-major, host or device memory; NULL =
+   * none).  When given, the
    * coarse solve is y = B0^{-1} c as an HBM-streaming GEMV (one right-hand
    * side) / FP64 tensor-core GEMM (batches) that runs beside the local
    * solves instead of the 2K-panel triangular chain.  The caller checks it
@@ -248,6 +249,10 @@ double hg_precond_stat(HgPrecond* p, int32_t key);
 int hg_precond_apply(HgPrecond* p, const double* r, double* out, void* stream);
 /* out = M^{-1} (B u) */
 int hg_precond_apply_T(HgPrecond* p, const double* u, double* out, void* stream);
+/* y = B0^{-1} c on the device's panel chain (c, y: device, length m): the
+ * coarse solve alone (lu_solve(b0_piv, c), schwarz.py:56), for the check
+ * factorize runs against getrs and for tests. */
+int hg_precond_coarse_solve(HgPrecond* p, const double* c, double* y, void* stream);
 /* out = Z B0^{-1} Z^T r (zeros without a coarse space) */
 int hg_precond_apply_coarse(HgPrecond* p, const double* r, double* out, void* stream);
 /* y = B x (which = 0) or y = D_k x (which = 1) */

@@ -128,6 +128,7 @@ SIGNATURES = {
     "hg_debug_set": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int64]),
     "hg_precond_read": (ctypes.c_int, [_vp, ctypes.c_int32, _f64p, ctypes.c_int64]),
     "hg_precond_stat": (ctypes.c_double, [_vp, ctypes.c_int32]),
+    "hg_precond_coarse_solve": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "hg_coarse_setup": (
         ctypes.c_int,
         [ctypes.POINTER(HgPrecondDesc), _i32p, _i32p, _f64p, _f64p, _i32p, _i32p, _f64p, ctypes.c_int32],

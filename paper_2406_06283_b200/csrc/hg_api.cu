@@ -61,7 +61,8 @@ static int upload(T** dptr, const T* host, size_t count, long long* bytes) {
   *dptr = nullptr;
   if (count == 0) return HG_OK;
   HG_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(dptr), sizeof(T) * count));
-  if (host) HG_CUDA_TRY(cudaMemcpy(*dptr, host, sizeof(T) * count, cudaMemcpyHostToDevice));
+  // cudaMemcpyDefault: descriptor arrays may be host or device memory (unified addressing)
+  if (host) HG_CUDA_TRY(cudaMemcpy(*dptr, host, sizeof(T) * count, cudaMemcpyDefault));
   if (bytes) *bytes += (long long)(sizeof(T) * count);
   return HG_OK;
 }
@@ -1292,6 +1293,46 @@ double hg_precond_stat(HgPrecond* P, int32_t key) {
     default:
       return NAN;
   }
+}
+
+// Z^T r partials that reduce to c (chunk 0 of each block = its part of c)
+__global__ void k_set_cpart(int m, const int* __restrict__ col_blk, const CblkDesc* __restrict__ descs,
+                            const double* __restrict__ c, double* __restrict__ cpart) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const CblkDesc d = descs[col_blk[i]];
+  const int l = i - d.col0;
+  for (int ch = 0; ch < d.nchunk; ++ch) cpart[d.part_off + (long long)ch * d.m + l] = ch == 0 ? c[i] : 0.0;
+}
+
+// the completion counts one Z^T r launch leaves behind (what the paired coarse solve waits for)
+__global__ void k_count_zt(int nblk, const CblkDesc* __restrict__ descs, unsigned long long* blk_done,
+                           unsigned long long* zt_done, unsigned long long nitems) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nblk) atomicAdd(blk_done + b, (unsigned long long)descs[b].nchunk);
+  if (b == 0) atomicAdd(zt_done, nitems);
+}
+
+int hg_precond_coarse_solve(HgPrecond* P, const double* c, double* y, void* stream) {
+  if (!P || !c || !y || P->m == 0) {
+    set_error("hg_precond_coarse_solve: bad argument (or no coarse space)");
+    return HG_ERR_ARG;
+  }
+  HG_TRY(precond_fault(P));
+  cudaStream_t st = (cudaStream_t)stream;
+  int s = HG_OK;
+  k_set_cpart<<<ceil_div(P->m, 256), 256, 0, st>>>(P->m, P->d_col_blk, P->d_cblk, c, P->d_cpart);
+  if (cudaGetLastError() != cudaSuccess) s = HG_ERR_CUDA;
+  if (s == HG_OK) {
+    k_count_zt<<<ceil_div(P->n_cblk, 256), 256, 0, st>>>(P->n_cblk, P->d_cblk, P->d_blk_done, P->d_zt_done,
+                                                         (unsigned long long)P->n_zt_items);
+    if (cudaGetLastError() != cudaSuccess) s = HG_ERR_CUDA;
+  }
+  if (s == HG_OK) s = launch_coarse_solve(P, st);  // the panel chain, whatever the apply mode
+  if (s == HG_OK && cudaMemcpyAsync(y, P->d_y, sizeof(double) * P->m, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    s = HG_ERR_CUDA;
+  if (s == HG_ERR_CUDA && hg::g_err.empty()) set_error("hg_precond_coarse_solve: launch failed");
+  return poison(P, s);
 }
 
 int hg_precond_spmv(HgPrecond* P, int which, const double* x, double* y, void* stream) {

@@ -59,26 +59,48 @@ __global__ void k_clear_zcols(const CsBlock* __restrict__ blk, int b, int nc, co
   X[(long long)(e % nc) * n + idx[d.idx_off + e / nc]] = 0.0;
 }
 
-// one CTA per interacting block a: out (l, c) = sum_k Z_a[k, l] Y[c][idof_a[k]]
-__global__ void __launch_bounds__(256) k_zty(const CsBlock* __restrict__ blk, const int* __restrict__ nbr,
-                                             const int* __restrict__ idx, const double* __restrict__ Z,
-                                             const double* __restrict__ Y, long long n, int nc, int colb,
-                                             double* __restrict__ B0, int m) {
-  const CsBlock d = blk[nbr[blockIdx.x]];
-  const int nout = d.m * nc;
-  for (int o = threadIdx.x; o < nout; o += blockDim.x) {
+constexpr int ZTY_ROWS = 64;   // rows of Z_a per partial-sum CTA
+constexpr int ZTY_MAXM = 64;   // coarse columns per block supported by the staged tile
+
+// partial (l, c) = sum_{k in chunk} Z_a[k, l] Y[c][idof_a[k]] for interacting block
+// a = nbr[blockIdx.y], rows chunk blockIdx.x; tiles staged in shared memory
+__global__ void __launch_bounds__(256) k_zty_part(const CsBlock* __restrict__ blk, const int* __restrict__ nbr,
+                                                  const int* __restrict__ idx, const double* __restrict__ Z,
+                                                  const double* __restrict__ Y, long long n, int nc,
+                                                  double* __restrict__ part, int nchunk_max) {
+  __shared__ double sz[ZTY_ROWS][ZTY_MAXM + 1];
+  __shared__ double sy[ZTY_ROWS][HG_MAX_RHS + 1];
+  const CsBlock d = blk[nbr[blockIdx.y]];
+  const int k0 = blockIdx.x * ZTY_ROWS;
+  double* out = part + ((long long)blockIdx.y * nchunk_max + blockIdx.x) * (ZTY_MAXM * HG_MAX_RHS);
+  if (k0 >= d.n) {
+    for (int o = threadIdx.x; o < d.m * nc; o += blockDim.x) out[o] = 0.0;
+    return;
+  }
+  const int rows = min(ZTY_ROWS, d.n - k0);
+  for (int e = threadIdx.x; e < rows * d.m; e += blockDim.x) sz[e / d.m][e % d.m] = Z[d.z_off + (long long)(k0 + e / d.m) * d.m + e % d.m];
+  for (int e = threadIdx.x; e < rows * nc; e += blockDim.x) {
+    const int k = e / nc, c = e % nc;
+    sy[k][c] = Y[(long long)c * n + idx[d.idx_off + k0 + k]];
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < d.m * nc; o += blockDim.x) {
     const int l = o / nc, c = o % nc;
-    const double* z = Z + d.z_off + l;
-    const double* y = Y + (long long)c * n;
-    const int* ix = idx + d.idx_off;
-    double s0 = 0.0, s1 = 0.0;
-    int k = 0;
-    for (; k + 1 < d.n; k += 2) {
-      s0 = fma(z[(long long)k * d.m], y[ix[k]], s0);
-      s1 = fma(z[(long long)(k + 1) * d.m], y[ix[k + 1]], s1);
-    }
-    if (k < d.n) s0 = fma(z[(long long)k * d.m], y[ix[k]], s0);
-    B0[(long long)(d.col0 + l) * m + colb + c] = s0 + s1;
+    double s = 0.0;
+    for (int k = 0; k < rows; ++k) s = fma(sz[k][l], sy[k][c], s);
+    out[o] = s;
+  }
+}
+
+// B0[col0_a + l, colb + c] = sum of the chunk partials in chunk order (deterministic)
+__global__ void k_zty_reduce(const CsBlock* __restrict__ blk, const int* __restrict__ nbr, int nc, int colb,
+                             const double* __restrict__ part, int nchunk_max, double* __restrict__ B0, int m) {
+  const CsBlock d = blk[nbr[blockIdx.x]];
+  const int nch = (d.n + ZTY_ROWS - 1) / ZTY_ROWS;
+  for (int o = threadIdx.x; o < d.m * nc; o += blockDim.x) {
+    double s = 0.0;
+    for (int ch = 0; ch < nch; ++ch) s += part[((long long)blockIdx.x * nchunk_max + ch) * (ZTY_MAXM * HG_MAX_RHS) + o];
+    B0[(long long)(d.col0 + o / nc) * m + colb + o % nc] = s;
   }
 }
 
@@ -227,28 +249,33 @@ __global__ void __launch_bounds__(256) k_gemv(const double* __restrict__ A, int 
   if (lane == 0) y[row] = s;
 }
 
-// one 64-row block of a triangular solve with the LU (L: unit lower; U: upper,
-// in reverse block order): x_t = D_t^{-1} (b_t - sum_{j != t, done} A[t, j] x_j)
+// off-diagonal part of block t of a triangular solve: x[r0 + i] -= A[r0 + i, done] x[done],
+// one warp per (row, 1/8 of the columns) with coalesced row reads; partials summed in order
+__global__ void __launch_bounds__(256) k_lu_solve_offdiag(const double* __restrict__ LU, int m, int t, bool upper,
+                                                          const double* __restrict__ x, double* __restrict__ part) {
+  const int r0 = t * CS_NB, rb = min(CS_NB, m - r0);
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31, seg = blockIdx.y;
+  if (row >= rb) return;
+  const int k0 = upper ? r0 + rb : 0, k1 = upper ? m : r0;
+  const int len = k1 - k0, per = (len + 7) / 8;
+  const int a0 = k0 + seg * per, a1 = min(k1, a0 + per);
+  const double* a = LU + (long long)(r0 + row) * m;
+  double s = 0.0;
+  for (int k = a0 + lane; k < a1; k += 32) s = fma(a[k], x[k], s);
+  s = warp_sum(s);
+  if (lane == 0) part[seg * CS_NB + row] = s;
+}
+
+// diagonal block t: x_t = D_t^{-1} (b_t - sum of the 8 partials)
 __global__ void __launch_bounds__(256) k_lu_solve_block(const double* __restrict__ LU, int m, int t, bool upper,
-                                                        double* __restrict__ x) {
-  __shared__ double part[4][CS_NB];
+                                                        double* __restrict__ x, const double* __restrict__ part) {
   __shared__ double xb[CS_NB];
   const int r0 = t * CS_NB, rb = min(CS_NB, m - r0);
-  const int row = threadIdx.x & 63, qq = threadIdx.x >> 6;  // 4 threads per row
-  double s = 0.0;
-  if (row < rb) {
-    const double* a = LU + (long long)(r0 + row) * m;
-    if (!upper) {
-      for (int k = qq; k < r0; k += 4) s = fma(a[k], x[k], s);
-    } else {
-      for (int k = r0 + rb + qq; k < m; k += 4) s = fma(a[k], x[k], s);
-    }
-  }
-  part[qq][row] = s;
-  __syncthreads();
   if (threadIdx.x < CS_NB) {
     const int i = threadIdx.x;
-    xb[i] = i < rb ? x[r0 + i] - ((part[0][i] + part[1][i]) + (part[2][i] + part[3][i])) : 0.0;
+    double s = 0.0;
+    for (int g = 0; g < 8; ++g) s += part[g * CS_NB + i];
+    xb[i] = i < rb ? x[r0 + i] - s : 0.0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {  // the diagonal block, sequentially
@@ -369,6 +396,17 @@ extern "C" int hg_coarse_setup(const HgPrecondDesc* D, const int32_t* pair_ptr, 
   HG_TRY(B.add<double>(&d_B0, nullptr, (size_t)m * m));
   HG_CUDA_TRY(cudaMemset(d_X, 0, sizeof(double) * (size_t)n * CW));
   HG_CUDA_TRY(cudaMemset(d_B0, 0, sizeof(double) * (size_t)m * m));
+  int nchunk_max = 1, nbr_max = 1;
+  for (int b = 0; b < nb; ++b) {
+    if (blk[b].m > ZTY_MAXM) {
+      set_error("hg_coarse_setup: more than 64 coarse columns in one block");
+      return HG_ERR_UNSUPPORTED;
+    }
+    nchunk_max = std::max(nchunk_max, ceil_div(blk[b].n, ZTY_ROWS));
+    nbr_max = std::max(nbr_max, pair_ptr[b + 1] - pair_ptr[b]);
+  }
+  double* d_part = nullptr;
+  HG_TRY(B.add<double>(&d_part, nullptr, (size_t)nbr_max * nchunk_max * ZTY_MAXM * HG_MAX_RHS));
   cudaStream_t st = 0;
   // ---- B0 = Z^T (B Z), 16 columns of one block at a time
   for (int b = 0; b < nb; ++b) {
@@ -380,7 +418,11 @@ extern "C" int hg_coarse_setup(const HgPrecondDesc* D, const int32_t* pair_ptr, 
       HG_LAUNCH_CHECK();
       HG_TRY(launch_spmm(A, A.data, d_X, n, d_Y, n, nc, st));
       if (na > 0) {
-        k_zty<<<na, 256, 0, st>>>(d_blk, d_nbr + pair_ptr[b], d_idx, d_z, d_Y, n, nc, blk[b].col0 + c0, d_B0, m);
+        k_zty_part<<<dim3(nchunk_max, na), 256, 0, st>>>(d_blk, d_nbr + pair_ptr[b], d_idx, d_z, d_Y, n, nc, d_part,
+                                                         nchunk_max);
+        HG_LAUNCH_CHECK();
+        k_zty_reduce<<<na, 256, 0, st>>>(d_blk, d_nbr + pair_ptr[b], nc, blk[b].col0 + c0, d_part, nchunk_max, d_B0,
+                                          m);
         HG_LAUNCH_CHECK();
       }
       k_clear_zcols<<<ceil_div(ne, 256), 256, 0, st>>>(d_blk, b, nc, d_idx, d_X, n);
@@ -461,15 +503,23 @@ extern "C" int hg_coarse_setup(const HgPrecondDesc* D, const int32_t* pair_ptr, 
     for (int i = 0; i < m; ++i)
       if (hpiv[i] != i) std::swap(perm[i], perm[hpiv[i]]);  // (P b)[i] = b[perm[i]] (getrs row interchanges)
     int* d_perm = nullptr;
+    double* d_sp = nullptr;  // 8 x 64 partial sums of one block's off-diagonal rows
     HG_TRY(B.add(&d_perm, perm.data(), (size_t)m));
+    HG_TRY(B.add<double>(&d_sp, nullptr, 8 * CS_NB));
     for (double& v : hx) v = rnd();
     const int K = ceil_div(m, CS_NB);
     for (int it = 0; it < iters; ++it) {
       const double nx = host_norm(hx);
       HG_CUDA_TRY(cudaMemcpy(d_x, hx.data(), sizeof(double) * m, cudaMemcpyHostToDevice));
       k_gather<<<ceil_div(m, 256), 256, 0, st>>>(d_perm, m, d_x, d_y);  // getrs: row interchanges first
-      for (int t = 0; t < K; ++t) k_lu_solve_block<<<1, 256, 0, st>>>(d_LU, m, t, false, d_y);
-      for (int t = K - 1; t >= 0; --t) k_lu_solve_block<<<1, 256, 0, st>>>(d_LU, m, t, true, d_y);
+      for (int t = 0; t < K; ++t) {
+        k_lu_solve_offdiag<<<dim3(8, 8), 256, 0, st>>>(d_LU, m, t, false, d_y, d_sp);
+        k_lu_solve_block<<<1, 256, 0, st>>>(d_LU, m, t, false, d_y, d_sp);
+      }
+      for (int t = K - 1; t >= 0; --t) {
+        k_lu_solve_offdiag<<<dim3(8, 8), 256, 0, st>>>(d_LU, m, t, true, d_y, d_sp);
+        k_lu_solve_block<<<1, 256, 0, st>>>(d_LU, m, t, true, d_y, d_sp);
+      }
       HG_LAUNCH_CHECK();
       HG_CUDA_TRY(cudaMemcpy(hy.data(), d_y, sizeof(double) * m, cudaMemcpyDeviceToHost));
       const double ny = host_norm(hy);

@@ -297,6 +297,15 @@ class TwoLevelPreconditioner:
         t0 = self._t()
         self._create(arrays, meta)  # upload + device band LU + panel records
         self.setup_times["create"] = self._t() - t0
+        if self.m:
+            t0 = self._t()
+            meta["b0_tile_dev"] = self.b0_tile_dev = self._check_coarse_solve()
+            self.setup_times["b0_guard"] = self._t() - t0
+        if "b0_inv" in arrays and not isinstance(arrays["b0_inv"], np.ndarray):  # device copy: host only if cached
+            arrays = dict(arrays)
+            binv = arrays.pop("b0_inv")
+            if self._keep_image:
+                arrays["b0_inv"] = binv.cpu().numpy()
         if "factor_info" in arrays:
             self._check_device_factor(arrays, meta)
             if self._keep_image:  # the cache stores the device-built records, not the factor inputs
@@ -457,24 +466,15 @@ class TwoLevelPreconditioner:
                 mode = 0
             if mode == 1:
                 T = T.premultiply()  # tiles D_t^{-1} T[t, j]: rows of a panel finish independently
-            # guard: the tiled algorithm (inverted diagonal blocks) must agree with getrs on several
-            # vectors (a getrs-equivalent operator: explicit inverses of 64x64 blocks)
             self.setup_times["b0_tiles"] = self._t() - t0
-            t0 = self._t()
-            rng = np.random.default_rng(0)
-            dev = 0.0
-            for _ in range(4):
-                c = rng.standard_normal(m)
-                want = scipy.linalg.lu_solve((lu, piv), c)
-                dev = max(dev, float(np.abs(T.solve(c) - want).max() / max(np.abs(want).max(), 1e-300)))
-            if dev > 1e-11:
-                raise SingularOperatorError(
-                    "coarse tile factorisation deviates from getrs by %.2e (B0 too ill-conditioned for "
-                    "inverted %dx%d diagonal blocks)" % (dev, P, P))
+            # the tiled algorithm (inverted 64x64 diagonal blocks) is checked against getrs on
+            # the device kernel itself once the handle exists (_check_coarse_solve); the host-only image
+            # (no device) checks the host emulation of the same algorithm
             self.b0_tiles = T
-            self.setup_times["b0_guard"] = self._t() - t0
+            self._b0_lu = (lu, piv)
+            if getattr(self, "_host_only", False):
+                M["b0_tile_dev"] = self._tile_guard(lambda c: T.solve(c), lu, piv, m, P)
             t0 = self._t()
-            M["b0_tile_dev"] = dev
             M["b0_bytes"] = int(T.nbytes + 4 * m + 4 * T.tile_col.size)
             # dense mode: B0^{-1} applied as a streaming GEMV / DMMA GEMM beside the
             # local solves; kept only if it agrees with getrs (the reference's lu_solve)
@@ -485,21 +485,23 @@ class TwoLevelPreconditioner:
             host_only = getattr(self, "_host_only", False)  # host_image(): no device to invert on
             dense = os.environ.get("HG_B0_DENSE", "multi" if m <= 20000 and not host_only else "0")
             if dense in ("1", "multi") or (dense == "auto" and m <= 20000):  # "auto": whenever it fits
+                # B0^{-1} on the device (setup; stays there: hg_precond_create copies device to device),
+                # checked against getrs (the reference's lu_solve) on two seeded vectors
                 torch = _torch()
                 B0 = np.ascontiguousarray(np.asarray(self._coarse.B0), dtype=np.float64)
                 Binv = torch.linalg.inv(torch.from_numpy(B0).cuda())
-                Binv = np.ascontiguousarray(Binv.cpu().numpy())
                 rng = np.random.default_rng(1)
                 ddev = 0.0
                 for _ in range(2):
                     c = rng.standard_normal(m)
                     want = scipy.linalg.lu_solve((lu, piv), c)
-                    ddev = max(ddev, float(np.abs(Binv @ c - want).max() / max(np.abs(want).max(), 1e-300)))
+                    got = (Binv @ torch.from_numpy(c).cuda()).cpu().numpy()
+                    ddev = max(ddev, float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-300)))
                 M["b0_dense_dev"] = ddev
                 if ddev <= 1e-11:
                     M["b0_dense"] = True
                     M["b0_inv_batched_only"] = 1 if dense == "multi" else 0
-                    put("b0_inv", Binv, f64)
+                    A["b0_inv"] = Binv.contiguous()
                     M["b0_bytes_multi"] = int(8 * m * m + 16 * m)
                     if dense != "multi":
                         M["b0_bytes"] = int(8 * m * m + 16 * m)
@@ -532,15 +534,51 @@ class TwoLevelPreconditioner:
             put("b0_tiles", tiles, f64)
         return A, M
 
+    @staticmethod
+    def _tile_guard(solve, lu, piv, m, P):
+        """Max relative deviation of a B0 solve from getrs on 4 seeded vectors;
+        raises SingularOperatorError above 1e-11 (B0 too ill-conditioned for the
+        inverted diagonal blocks of the tile algorithm)."""
+        rng = np.random.default_rng(0)
+        dev = 0.0
+        for _ in range(4):
+            c = rng.standard_normal(m)
+            want = scipy.linalg.lu_solve((lu, piv), c)
+            dev = max(dev, float(np.abs(solve(c) - want).max() / max(np.abs(want).max(), 1e-300)))
+        if dev > 1e-11:
+            raise SingularOperatorError(
+                "coarse tile factorisation deviates from getrs by %.2e (B0 too ill-conditioned for "
+                "inverted %dx%d diagonal blocks)" % (dev, P, P))
+        return dev
+
+    def _check_coarse_solve(self):
+        """The guard of the tiled coarse solve, run on the device chain kernel itself."""
+        torch = _torch()
+        lu, piv = self._b0_lu
+
+        def dev_solve(c):
+            cd = torch.from_numpy(c).cuda()
+            y = torch.empty_like(cd)
+            _lib.check(_lib.load().hg_precond_coarse_solve(self._handle, _vp(cd), _vp(y), _stream()),
+                       "hg_precond_coarse_solve")
+            return y.cpu().numpy()
+
+        return self._tile_guard(dev_solve, lu, piv, self.m, self.b0_tiles.P)
+
     def _create(self, arrays, meta):
         """hg_precond_create from an image (``_image`` or the setup cache)."""
         lib = _lib.load()
-        _torch()  # CUDA context present before the first allocation
+        torch = _torch()  # CUDA context present before the first allocation
         d = _lib.HgPrecondDesc()
         for name, ctype in _lib.HgPrecondDesc._fields_:
-            if issubclass(ctype, ctypes._Pointer):  # array field
+            if issubclass(ctype, ctypes._Pointer):  # array field (numpy host array or CUDA tensor)
                 a = arrays.get(name)
-                setattr(d, name, None if a is None else a.ctypes.data_as(ctype))
+                if a is None:
+                    setattr(d, name, None)
+                elif isinstance(a, torch.Tensor):
+                    setattr(d, name, ctypes.cast(ctypes.c_void_p(a.data_ptr()), ctype))
+                else:
+                    setattr(d, name, a.ctypes.data_as(ctype))
             else:
                 setattr(d, name, int(meta.get(name, 0)))
         h = ctypes.c_void_p()
