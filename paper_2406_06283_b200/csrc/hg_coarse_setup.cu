@@ -277,23 +277,26 @@ __global__ void __launch_bounds__(256) k_lu_solve_block(const double* __restrict
     for (int g = 0; g < 8; ++g) s += part[g * CS_NB + i];
     xb[i] = i < rb ? x[r0 + i] - s : 0.0;
   }
+  __shared__ double D[CS_NB][CS_NB + 1];  // the diagonal block, staged once
+  for (int e = threadIdx.x; e < rb * rb; e += blockDim.x) D[e / rb][e % rb] = LU[(long long)(r0 + e / rb) * m + r0 + e % rb];
   __syncthreads();
-  if (threadIdx.x == 0) {  // the diagonal block, sequentially
-    if (!upper) {
-      for (int i = 0; i < rb; ++i) {
-        double v = xb[i];
-        for (int k = 0; k < i; ++k) v = fma(-LU[(long long)(r0 + i) * m + r0 + k], xb[k], v);
-        xb[i] = v;
-      }
-    } else {
-      for (int i = rb - 1; i >= 0; --i) {
-        double v = xb[i];
-        for (int k = i + 1; k < rb; ++k) v = fma(-LU[(long long)(r0 + i) * m + r0 + k], xb[k], v);
-        xb[i] = v / LU[(long long)(r0 + i) * m + r0 + i];
-      }
+  // column-oriented substitution: step i finalises x_i, then every row below (L) / above (U) is updated
+  if (!upper) {
+    for (int i = 0; i < rb; ++i) {
+      const double xi = xb[i];
+      __syncthreads();
+      if (threadIdx.x > i && threadIdx.x < rb) xb[threadIdx.x] = fma(-D[threadIdx.x][i], xi, xb[threadIdx.x]);
+      __syncthreads();
+    }
+  } else {
+    for (int i = rb - 1; i >= 0; --i) {
+      if (threadIdx.x == 0) xb[i] = xb[i] / D[i][i];
+      __syncthreads();
+      const double xi = xb[i];
+      if (threadIdx.x < i) xb[threadIdx.x] = fma(-D[threadIdx.x][i], xi, xb[threadIdx.x]);
+      __syncthreads();
     }
   }
-  __syncthreads();
   if (threadIdx.x < rb) x[r0 + threadIdx.x] = xb[threadIdx.x];
 }
 

@@ -68,7 +68,17 @@ def solve_local_gevps_device(forms, dec, n_wanted, shift=2.0, tol=1e-15, max_res
     forms_bd = types.SimpleNamespace(helmholtz=Mbig, dk=Cbig, n_dofs=N, k=None)
     subs = [types.SimpleNamespace(idof=np.arange(offs[i], offs[i + 1]), diameter=np.nan) for i in range(nb)]
     dec_bd = types.SimpleNamespace(fine_flat=lambda: ((i, 0, subs[i]) for i in range(nb)))
-    pre = factorize(forms_bd, dec_bd, None)  # device band LU of every B_i + g C_i
+    import os
+
+    saved = os.environ.get("HG_LOCAL_PANEL")
+    os.environ["HG_LOCAL_PANEL"] = "0"  # single-vector applies only: no batched panel records
+    try:
+        pre = factorize(forms_bd, dec_bd, None)  # device band LU of every B_i + g C_i
+    finally:
+        if saved is None:
+            del os.environ["HG_LOCAL_PANEL"]
+        else:
+            os.environ["HG_LOCAL_PANEL"] = saved
 
     dev = torch.device("cuda")
     f64 = torch.float64

@@ -473,7 +473,7 @@ class TwoLevelPreconditioner:
             self.b0_tiles = T
             self._b0_lu = (lu, piv)
             if getattr(self, "_host_only", False):
-                M["b0_tile_dev"] = self._tile_guard(lambda c: T.solve(c), lu, piv, m, P)
+                M["b0_tile_dev"] = self._tile_guard(lambda c: T.solve(c), m, P)
             t0 = self._t()
             M["b0_bytes"] = int(T.nbytes + 4 * m + 4 * T.tile_col.size)
             # dense mode: B0^{-1} applied as a streaming GEMV / DMMA GEMM beside the
@@ -492,9 +492,10 @@ class TwoLevelPreconditioner:
                 Binv = torch.linalg.inv(torch.from_numpy(B0).cuda())
                 rng = np.random.default_rng(1)
                 ddev = 0.0
+                getrs = self._getrs()
                 for _ in range(2):
                     c = rng.standard_normal(m)
-                    want = scipy.linalg.lu_solve((lu, piv), c)
+                    want = getrs(c)
                     got = (Binv @ torch.from_numpy(c).cuda()).cpu().numpy()
                     ddev = max(ddev, float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-300)))
                 M["b0_dense_dev"] = ddev
@@ -534,16 +535,36 @@ class TwoLevelPreconditioner:
             put("b0_tiles", tiles, f64)
         return A, M
 
-    @staticmethod
-    def _tile_guard(solve, lu, piv, m, P):
+    def _getrs(self):
+        """c -> getrs(lu, piv, c) (the reference's lu_solve, schwarz.py:56) with the
+        same getrf factors; on the device when there is one (the factors are
+        uploaded once per factorize), else LAPACK."""
+        if getattr(self, "_getrs_fn", None) is not None:
+            return self._getrs_fn
+        lu, piv = self._b0_lu
+        if getattr(self, "_host_only", False):
+            fn = lambda c: scipy.linalg.lu_solve((lu, piv), c)  # noqa: E731
+        else:
+            torch = _torch()
+            LU = torch.from_numpy(np.ascontiguousarray(lu)).cuda()
+            pv = torch.from_numpy(np.asarray(piv, dtype=np.int32) + 1).cuda()  # LAPACK 1-based
+
+            def fn(c):
+                b = torch.from_numpy(np.ascontiguousarray(c, dtype=np.float64)).cuda()[:, None]
+                return torch.linalg.lu_solve(LU, pv, b)[:, 0].cpu().numpy()
+        self._getrs_fn = fn
+        return fn
+
+    def _tile_guard(self, solve, m, P):
         """Max relative deviation of a B0 solve from getrs on 4 seeded vectors;
         raises SingularOperatorError above 1e-11 (B0 too ill-conditioned for the
         inverted diagonal blocks of the tile algorithm)."""
         rng = np.random.default_rng(0)
         dev = 0.0
+        getrs = self._getrs()
         for _ in range(4):
             c = rng.standard_normal(m)
-            want = scipy.linalg.lu_solve((lu, piv), c)
+            want = getrs(c)
             dev = max(dev, float(np.abs(solve(c) - want).max() / max(np.abs(want).max(), 1e-300)))
         if dev > 1e-11:
             raise SingularOperatorError(
@@ -554,7 +575,6 @@ class TwoLevelPreconditioner:
     def _check_coarse_solve(self):
         """The guard of the tiled coarse solve, run on the device chain kernel itself."""
         torch = _torch()
-        lu, piv = self._b0_lu
 
         def dev_solve(c):
             cd = torch.from_numpy(c).cuda()
@@ -563,7 +583,9 @@ class TwoLevelPreconditioner:
                        "hg_precond_coarse_solve")
             return y.cpu().numpy()
 
-        return self._tile_guard(dev_solve, lu, piv, self.m, self.b0_tiles.P)
+        res = self._tile_guard(dev_solve, self.m, self.b0_tiles.P)
+        self._getrs_fn = None  # the device copy of the factors is not kept
+        return res
 
     def _create(self, arrays, meta):
         """hg_precond_create from an image (``_image`` or the setup cache)."""
