@@ -1050,9 +1050,19 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
     HG_CUDA_TRY(cudaMemset(P->d_blk_done, 0, sizeof(unsigned long long) * D->n_cblk));
     HG_TRY(upload<double>(&P->d_y, nullptr, (size_t)P->m, bytes));
     if (D->b0_inv) {
-      HG_TRY(upload(&P->d_b0_inv, D->b0_inv, (size_t)P->m * P->m, bytes));
+      // row-major in (host or device memory), kept packed in DMMA-fragment order
+      double* rowmajor = nullptr;
+      cudaPointerAttributes pa{};
+      const bool on_dev = cudaPointerGetAttributes(&pa, D->b0_inv) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+      cudaGetLastError();
+      if (!on_dev) HG_TRY(upload(&rowmajor, D->b0_inv, (size_t)P->m * P->m, nullptr));
+      const int ps = pack_b0_inverse(P->m, on_dev ? D->b0_inv : rowmajor, &P->d_b0_inv, &P->b0_mp);
+      release(rowmajor);
+      HG_TRY(ps);
+      if (bytes) *bytes += (long long)sizeof(double) * P->b0_mp * P->b0_mp;
       P->b0_inv_single = D->b0_inv_batched_only == 0;
-      HG_TRY(upload<double>(&P->d_c, nullptr, (size_t)P->m, bytes));
+      HG_TRY(upload<double>(&P->d_c, nullptr, (size_t)P->b0_mp, bytes));
+      HG_CUDA_TRY(cudaMemset(P->d_c, 0, sizeof(double) * P->b0_mp));
     }
     HG_TRY(upload<double>(&P->d_zs, nullptr, (size_t)std::max(nidx, 1LL), bytes));
     std::vector<int> ptr;

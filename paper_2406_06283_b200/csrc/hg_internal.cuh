@@ -99,7 +99,8 @@ struct HgPrecond {
   int* d_fault = nullptr;
   int skip_zt = 0;                // fault injection (hg_debug_set): Z^T r launches to drop
   double* d_y = nullptr;          // coarse solution (m)
-  double* d_b0_inv = nullptr;     // dense B0^{-1} (m x m row-major) or null
+  double* d_b0_inv = nullptr;     // dense B0^{-1}, packed 8 x 8 fragment blocks (hg_b0d.cu), b0_mp x b0_mp, or null
+  int b0_mp = 0;                  // m rounded up to 8
   bool b0_inv_single = true;      // single-RHS applies use it too (else only the batched ones)
   double* d_c = nullptr;          // reduced Z^T r (m), dense mode
   double* d_cm = nullptr;         // [m][16] reduced Z^T R, dense mode
@@ -233,7 +234,8 @@ int launch_b0_multi(HgPrecond* P, int nrhs, cudaStream_t st);
 int launch_b0_dense(HgPrecond* P, cudaStream_t st);
 int launch_b0_dense_multi(HgPrecond* P, int nrhs, cudaStream_t st);
 int preload_b0_dense();
-constexpr int B0_KSPLIT = 4;
+int pack_b0_inverse(int m, const double* d_binv, double** d_packed, int* mp_out);
+constexpr int B0_KSPLIT = 8;
 int launch_zy_multi(HgPrecond* P, int nrhs, cudaStream_t st);
 int launch_assemble_multi(HgPrecond* P, bool with_coarse, bool with_local, double* OUT, long long ldo, int nrhs,
                           cudaStream_t st);

@@ -34,7 +34,13 @@ namespace hg {
 
 namespace {
 constexpr int PB = 16;        // panel rows
-constexpr int PSR = 20;       // window row stride (16 columns + pad: conflict-free B fragments)
+// window row stride for NT column tiles of 8 (+ pad: conflict-free B fragments; (stride q + g) mod 16
+// distinct over a half-warp for stride 20 and 12)
+template <int NT>
+struct PanelCols {
+  static constexpr int NC = 8 * NT;
+  static constexpr int PSR = NT == 2 ? 20 : 12;
+};
 constexpr int PNS_MAX = 8;    // ring stages (runtime count ns <= PNS_MAX: PanelArgs::ns)
 constexpr int PD = 4;         // panels of look-ahead for the entering rows (a gather is two dependent loads)
 constexpr int PTHREADS = 256 + 32;
@@ -197,12 +203,14 @@ struct PanelSweep {
   int n, kwp, WR, mtT;
   int* chunk;
   const unsigned char* mt;   // this sweep's per-panel m-tile counts (shared memory)
+  const double* R;           // this CTA's first column of the batch
+  int nr;                    // this CTA's column count (<= 8 NT)
 };
 
 template <bool FWD>
 __device__ __forceinline__ double panel_in(const PanelSweep& S, int row, int c) {
-  if (row >= S.n || c >= S.a->nrhs) return 0.0;
-  if (FWD) return __ldg(S.a->R + (long long)c * S.a->ldr + __ldg(S.idx + row));
+  if (row >= S.n || c >= S.nr) return 0.0;
+  if (FWD) return __ldg(S.R + (long long)c * S.a->ldr + __ldg(S.idx + row));
   return S.xs[(long long)c * S.a->xs_len + (S.n - 1 - row)];
 }
 
@@ -212,33 +220,38 @@ __device__ __forceinline__ int panel_idx(const PanelSweep& S, int row) { return 
 
 template <bool FWD>
 __device__ __forceinline__ double panel_val(const PanelSweep& S, int row, int c, int gi) {
-  if (row >= S.n || c >= S.a->nrhs) return 0.0;
-  if (FWD) return __ldg(S.a->R + (long long)c * S.a->ldr + gi);
+  if (row >= S.n || c >= S.nr) return 0.0;
+  if (FWD) return __ldg(S.R + (long long)c * S.a->ldr + gi);
   return S.xs[(long long)c * S.a->xs_len + (S.n - 1 - row)];
 }
 
 // window row (j0 + off) for 0 <= off < WR, given base = j0 mod WR
+template <int NT>
 __device__ __forceinline__ double* panel_row(const PanelSweep& S, int base, int off) {
   int r = base + off;
   if (r >= S.WR) r -= S.WR;
-  return S.W + (size_t)r * PSR;
+  return S.W + (size_t)r * PanelCols<NT>::PSR;
 }
 
 // One panel p.  `ev` is this panel's slot of the entering-row look-ahead: it
 // holds the value loaded PD panels ago (stored into the window here) and is
 // refilled for panel p + PD — a fixed register per slot (the caller unrolls
 // PD panels), so no in-flight load is ever moved between registers.
-template <bool FWD>
+template <bool FWD, int NT>
 __device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& ev, int& ei) {
+  constexpr int NC = PanelCols<NT>::NC;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, q = lane & 3, g = lane >> 2;
-  const int er = tid >> 4, ec = tid & 15;
+  const int er = tid / NC, ec = tid % NC;
+  const bool eact = tid < PB * NC;  // threads that carry an entering-row element
   const int kwp = S.kwp;
   const int j0 = p * PB;
   const int base = j0 % S.WR;
   const double evc = ev;
   const int erow = j0 + PB + kwp + er;
-  ev = panel_val<FWD>(S, erow + PB * PD, ec, ei);       // value for panel p + PD (its index loaded PD panels ago)
-  if (FWD) ei = panel_idx(S, erow + 2 * PB * PD);       // index for panel p + 2 PD
+  if (eact) {
+    ev = panel_val<FWD>(S, erow + PB * PD, ec, ei);     // value for panel p + PD (its index loaded PD panels ago)
+    if (FWD) ei = panel_idx(S, erow + 2 * PB * PD);     // index for panel p + 2 PD
+  }
   const int chunk = *S.chunk;
   const int ns = S.a->ns;
   const int stage = chunk % ns;
@@ -257,9 +270,9 @@ __device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& e
       if (warp == 0) {
         for (int t = 0; t < PB; ++t) {
           const int p2 = __double2int_rn(rec[t]);
-          if (p2 != t && lane < 16) {
-            double* r1 = panel_row(S, base, t);
-            double* r2 = panel_row(S, base, p2);
+          if (p2 != t && lane < NC) {
+            double* r1 = panel_row<NT>(S, base, t);
+            double* r2 = panel_row<NT>(S, base, p2);
             const double tmp = r1[lane];
             r1[lane] = r2[lane];
             r2[lane] = tmp;
@@ -274,16 +287,16 @@ __device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& e
   double b0[4], b1[4];
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
-    const double* wr = panel_row(S, base, ks * 4 + q);
+    const double* wr = panel_row<NT>(S, base, ks * 4 + q);
     b0[ks] = wr[g];
-    b1[ks] = wr[8 + g];
+    b1[ks] = NT == 2 ? wr[8 + g] : 0.0;
   }
-  // tiles: 0..3 = X = D^{-1} W (2 m x 2 n); 4.. = trailing rows += -(T D^{-1}) W.
-  // Warp w takes tiles w, w+8, ... (all of the same n-tile, w & 1), at most
+  // tiles (m-tile t / NT, n-tile t % NT): m-tiles 0, 1 = X = D^{-1} W; 2.. = trailing rows
+  // += -(T D^{-1}) W.  Warp w takes tiles w, w+8, ... (all of the same n-tile), at most
   // TG of them, k-steps interleaved across its tiles.
-  const int ntile = 4 + 2 * mtp;
+  const int ntile = NT * (2 + mtp);
   constexpr int TG = 5;
-  const double* bsel = (warp & 1) ? b1 : b0;
+  const double* bsel = (NT == 2 && (warp & 1)) ? b1 : b0;
   // groups of TG tiles per warp (one group while ntile <= 40, i.e. kw <= 144)
   for (int t0 = warp; t0 < ntile; t0 += 8 * TG) {
     const int nu = min(TG, (ntile - t0 + 7) >> 3);  // tiles of this warp in this group
@@ -297,12 +310,13 @@ __device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& e
       crow[u] = nullptr;
       ap[u] = rec + lane;
       if (u < nu) {
-        if (t < 4) {
-          ap[u] = rec + 16 + (t >> 1) * 128 + lane;
+        const int tm = t / NT, tn = t % NT;
+        if (tm < 2) {
+          ap[u] = rec + 16 + tm * 128 + lane;
         } else {
-          const int mt = (t - 4) >> 1;
+          const int mt = tm - 2;
           ap[u] = rec + PREC_HDR + mt * 128 + lane;
-          crow[u] = panel_row(S, base, PB + mt * 8 + g) + (t & 1) * 8 + 2 * q;
+          crow[u] = panel_row<NT>(S, base, PB + mt * 8 + g) + tn * 8 + 2 * q;
           const double2 c2 = *reinterpret_cast<const double2*>(crow[u]);
           acc[u][0] = c2.x;
           acc[u][1] = c2.y;
@@ -319,12 +333,12 @@ __device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& e
     for (int u = 0; u < TG; ++u) {
       if (u >= nu) continue;
       const int t = t0 + 8 * u;
-      if (t < 4) {
-        const int r = (t >> 1) * 8 + g, c = (t & 1) * 8 + 2 * q;
+      if (t < 2 * NT) {
+        const int r = (t / NT) * 8 + g, c = (t % NT) * 8 + 2 * q;
         double* xs = S.xs + (FWD ? (long long)(j0 + r) : (long long)(S.n - 1 - (j0 + r)));
         if (j0 + r < S.n) {
-          if (c < S.a->nrhs) xs[(long long)c * S.a->xs_len] = acc[u][0];
-          if (c + 1 < S.a->nrhs) xs[(long long)(c + 1) * S.a->xs_len] = acc[u][1];
+          if (c < S.nr) xs[(long long)c * S.a->xs_len] = acc[u][0];
+          if (c + 1 < S.nr) xs[(long long)(c + 1) * S.a->xs_len] = acc[u][1];
         }
       } else {
         *reinterpret_cast<double2*>(crow[u]) = make_double2(acc[u][0], acc[u][1]);
@@ -332,33 +346,36 @@ __device__ __forceinline__ void panel_step(const PanelSweep& S, int p, double& e
     }
   }
   // entering rows take the slots of the previous panel (finished)
-  panel_row(S, base, PB + kwp + er)[ec] = evc;
+  if (eact) panel_row<NT>(S, base, PB + kwp + er)[ec] = evc;
   psync();
   if (tid == 0) mbar_arrive(&S.empty[stage]);
   *S.chunk = chunk + 1;
 }
 
-template <bool FWD>
+template <bool FWD, int NT>
 __device__ __forceinline__ void panel_sweep(const PanelArgs& a, const LocalDesc& d, double* ring, uint64_t* full,
-                                            uint64_t* empty, double* W, int& chunk) {
+                                            uint64_t* empty, double* W, int& chunk, int c0) {
+  constexpr int NC = PanelCols<NT>::NC;
   const int tid = threadIdx.x;
-  const unsigned char* smt = reinterpret_cast<const unsigned char*>(W + (size_t)a.WR * PSR);
-  PanelSweep S{&a, a.idx + d.idx_off, a.xs + d.idx_off, W, ring, full, empty, d.n, FWD ? a.kwf : a.kwb, a.WR, 0,
-               &chunk, smt + (FWD ? 0 : (d.n + PB - 1) / PB)};
+  const unsigned char* smt = reinterpret_cast<const unsigned char*>(W + (size_t)a.WR * PanelCols<NT>::PSR);
+  PanelSweep S{&a, a.idx + d.idx_off, a.xs + d.idx_off + (long long)c0 * a.xs_len, W, ring, full, empty, d.n,
+               FWD ? a.kwf : a.kwb, a.WR, 0, &chunk, smt + (FWD ? 0 : (d.n + PB - 1) / PB),
+               a.R + (long long)c0 * a.ldr, min(NC, a.nrhs - c0)};
   S.mtT = S.kwp >> 3;
   const int np = (S.n + PB - 1) / PB;
   // prologue: panel 0 and its trailing rows
-  for (int e = tid; e < (PB + S.kwp) * 16; e += 256) panel_row(S, 0, e >> 4)[e & 15] = panel_in<FWD>(S, e >> 4, e & 15);
+  for (int e = tid; e < (PB + S.kwp) * NC; e += 256) panel_row<NT>(S, 0, e / NC)[e % NC] = panel_in<FWD>(S, e / NC, e % NC);
   // rows entering at panels 0..PD-1, in flight ahead of their use (this
   // thread's row tid / 16, column tid % 16 of each 16-row group)
-  const int er = tid >> 4, ec = tid & 15;
+  const int er = tid / NC, ec = tid % NC;
+  const bool eact = tid < PB * NC;
   const int r0 = PB + S.kwp + er;
-  double ev0 = panel_in<FWD>(S, r0, ec);
-  double ev1 = panel_in<FWD>(S, r0 + PB, ec);
-  double ev2 = panel_in<FWD>(S, r0 + 2 * PB, ec);
-  double ev3 = panel_in<FWD>(S, r0 + 3 * PB, ec);
+  double ev0 = eact ? panel_in<FWD>(S, r0, ec) : 0.0;
+  double ev1 = eact ? panel_in<FWD>(S, r0 + PB, ec) : 0.0;
+  double ev2 = eact ? panel_in<FWD>(S, r0 + 2 * PB, ec) : 0.0;
+  double ev3 = eact ? panel_in<FWD>(S, r0 + 3 * PB, ec) : 0.0;
   int ei0 = 0, ei1 = 0, ei2 = 0, ei3 = 0;  // gather indices of panels 4..7 (forward sweep)
-  if (FWD) {
+  if (FWD && eact) {
     ei0 = panel_idx(S, r0 + 4 * PB);
     ei1 = panel_idx(S, r0 + 5 * PB);
     ei2 = panel_idx(S, r0 + 6 * PB);
@@ -367,18 +384,25 @@ __device__ __forceinline__ void panel_sweep(const PanelArgs& a, const LocalDesc&
   static_assert(PD == 4, "unrolled look-ahead slots");
   psync();
   for (int p = 0; p < np; p += PD) {
-    panel_step<FWD>(S, p, ev0, ei0);
-    if (p + 1 < np) panel_step<FWD>(S, p + 1, ev1, ei1);
-    if (p + 2 < np) panel_step<FWD>(S, p + 2, ev2, ei2);
-    if (p + 3 < np) panel_step<FWD>(S, p + 3, ev3, ei3);
+    panel_step<FWD, NT>(S, p, ev0, ei0);
+    if (p + 1 < np) panel_step<FWD, NT>(S, p + 1, ev1, ei1);
+    if (p + 2 < np) panel_step<FWD, NT>(S, p + 2, ev2, ei2);
+    if (p + 3 < np) panel_step<FWD, NT>(S, p + 3, ev3, ei3);
   }
 }
 
+// NT = 2: one CTA per block, 16 columns.  NT = 1: two CTAs per block, 8 columns each (the columns
+// are independent; the second read of the panel records comes from L2) — for decompositions with
+// fewer blocks than SMs.
+template <int NT>
 __global__ void __launch_bounds__(PTHREADS, 2) k_local_panel(PanelArgs a) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[PNS_MAX], empty[PNS_MAX];
   const int ns = a.ns;
-  const LocalDesc d = a.descs[blockIdx.x];
+  const int blk = NT == 2 ? blockIdx.x : blockIdx.x >> 1;
+  const int c0 = NT == 2 ? 0 : 8 * (blockIdx.x & 1);
+  if (c0 >= a.nrhs) return;
+  const LocalDesc d = a.descs[blk];
   if (threadIdx.x == 0) {
     for (int s = 0; s < ns; ++s) {
       mbar_init(&full[s], 1);
@@ -389,8 +413,9 @@ __global__ void __launch_bounds__(PTHREADS, 2) k_local_panel(PanelArgs a) {
   if (d.n == 0) return;
   const int np = (d.n + PB - 1) / PB;
   // per-panel m-tile counts of both sweeps into shared memory (after the window)
-  unsigned char* smt = reinterpret_cast<unsigned char*>(sm + (size_t)ns * a.stage_stride + (size_t)a.WR * PSR);
-  for (int e = threadIdx.x; e < 2 * np; e += blockDim.x) smt[e] = a.pmt[a.mtoff[blockIdx.x] + e];
+  unsigned char* smt =
+      reinterpret_cast<unsigned char*>(sm + (size_t)ns * a.stage_stride + (size_t)a.WR * PanelCols<NT>::PSR);
+  for (int e = threadIdx.x; e < 2 * np; e += blockDim.x) smt[e] = a.pmt[a.mtoff[blk] + e];
   __syncthreads();
   if (threadIdx.x >= 256) {
     if (threadIdx.x == 256) {  // producer: forward panels, then backward panels (used part only)
@@ -400,7 +425,7 @@ __global__ void __launch_bounds__(PTHREADS, 2) k_local_panel(PanelArgs a) {
         if (c >= ns) mbar_wait(&empty[stage], ((c / ns) - 1) & 1);
         const bool f = c < np;
         const int pp = f ? c : c - np;
-        const double* src = f ? a.pf + a.poff[2 * blockIdx.x] + pp * psf : a.pb + a.poff[2 * blockIdx.x + 1] + pp * psb;
+        const double* src = f ? a.pf + a.poff[2 * blk] + pp * psf : a.pb + a.poff[2 * blk + 1] + pp * psb;
         const uint32_t bytes = (uint32_t)(panel_used(smt[c]) * 8);
         mbar_arrive_expect_tx(&full[stage], bytes);
         bulk_g2s(sm + (size_t)stage * a.stage_stride, src, bytes, &full[stage]);
@@ -410,8 +435,8 @@ __global__ void __launch_bounds__(PTHREADS, 2) k_local_panel(PanelArgs a) {
   }
   double* W = sm + (size_t)ns * a.stage_stride;
   int chunk = 0;
-  panel_sweep<true>(a, d, sm, full, empty, W, chunk);
-  panel_sweep<false>(a, d, sm, full, empty, W, chunk);
+  panel_sweep<true, NT>(a, d, sm, full, empty, W, chunk, c0);
+  panel_sweep<false, NT>(a, d, sm, full, empty, W, chunk, c0);
 }
 
 // ------------------------------------------------------------------ host side
@@ -435,7 +460,7 @@ int launch_local_batch(HgPrecond* P, const double* R, long long ldr, int nrhs, c
 // 3), HG_PANEL_STAGES overrides (up to PNS_MAX; experiments)
 static int panel_stages(const HgPrecond* P) {
   const long long ss = std::max(panel_doubles(P->panel_kwf), panel_doubles(P->panel_kwb)) * 8;
-  const long long win = (long long)P->panel_wr * PSR * 8;
+  const long long win = (long long)P->panel_wr * PanelCols<2>::PSR * 8;
   static const int env = getenv("HG_PANEL_STAGES") ? atoi(getenv("HG_PANEL_STAGES")) : 0;
   if (env > 0) return std::min(env, PNS_MAX);
   const long long budget = 113 * 1024 - 256 - 2 * P->panel_np_max;  // two CTAs per SM
@@ -444,19 +469,33 @@ static int panel_stages(const HgPrecond* P) {
 
 static size_t panel_smem(const HgPrecond* P) {
   const long long ss = std::max(panel_doubles(P->panel_kwf), panel_doubles(P->panel_kwb));
-  return sizeof(double) * ((size_t)panel_stages(P) * ss + (size_t)P->panel_wr * PSR) +
+  return sizeof(double) * ((size_t)panel_stages(P) * ss + (size_t)P->panel_wr * PanelCols<2>::PSR) +
          (size_t)((2 * P->panel_np_max + 15) / 16 * 16);
 }
 
 int launch_local_panel(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st) {
   if (P->n_local == 0) return HG_OK;
   const size_t smem = panel_smem(P);
-  HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k_local_panel), smem, false));
+  // column split: two CTAs per block (8 columns each) while that still leaves every CTA resident
+  // (2 per SM); HG_PANEL_CSPLIT=0/1 overrides
+  static const int env = getenv("HG_PANEL_CSPLIT") ? atoi(getenv("HG_PANEL_CSPLIT")) : -1;
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const bool split = nrhs > 8 && (env >= 0 ? env != 0 : 2 * P->n_local <= 2 * sms);
+  const void* fn = split ? reinterpret_cast<const void*>(k_local_panel<1>)
+                         : reinterpret_cast<const void*>(k_local_panel<2>);
+  HG_TRY(ensure_func_attrs(fn, smem, false));
   PanelArgs a{P->d_local, P->d_poff, P->d_local_idx, P->d_pfwd, P->d_pbwd, R, ldr, P->d_xsm, P->xs_len, nrhs,
               P->panel_kwf, P->panel_kwb, P->panel_wr,
               (int)std::max(panel_doubles(P->panel_kwf), panel_doubles(P->panel_kwb)), panel_stages(P),
               P->d_pmt, P->d_mtoff, P->panel_np_max};
-  k_local_panel<<<P->n_local, PTHREADS, smem, st>>>(a);
+  if (split)
+    k_local_panel<1><<<2 * P->n_local, PTHREADS, smem, st>>>(a);
+  else
+    k_local_panel<2><<<P->n_local, PTHREADS, smem, st>>>(a);
   HG_LAUNCH_CHECK();
   return HG_OK;
 }
@@ -585,7 +624,8 @@ int prepare_local_panel(HgPrecond* P) {
 
 int preload_local_panel() {
   cudaFuncAttributes at;
-  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_local_panel));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_local_panel<1>));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_local_panel<2>));
   HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_panel_convert<true>));
   HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_panel_convert<false>));
   HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_fill_hash));

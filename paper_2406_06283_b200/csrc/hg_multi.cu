@@ -642,8 +642,9 @@ int multi_prepare(HgPrecond* P) {
     HG_TRY(alloc(&P->d_b0m_x, (size_t)2 * P->b0_K * BP * MR * 2));  // (value, tag) pairs
     HG_CUDA_TRY(cudaMemset(P->d_b0m_x, 0, sizeof(double) * 2 * P->b0_K * BP * MR * 2));  // tag 0 = never
     if (P->d_b0_inv) {
-      HG_TRY(alloc(&P->d_cm, (size_t)MR * P->m));
-      HG_TRY(alloc(&P->d_ypart, (size_t)B0_KSPLIT * MR * P->m));
+      HG_TRY(alloc(&P->d_cm, (size_t)MR * P->b0_mp));
+      HG_CUDA_TRY(cudaMemset(P->d_cm, 0, sizeof(double) * MR * P->b0_mp));  // rows beyond m stay zero
+      HG_TRY(alloc(&P->d_ypart, (size_t)B0_KSPLIT * MR * P->b0_mp));
     }
     HG_CUDA_TRY(cudaMalloc(&P->d_blkm_done, sizeof(unsigned long long) * P->n_cblk));
     HG_CUDA_TRY(cudaMemset(P->d_blkm_done, 0, sizeof(unsigned long long) * P->n_cblk));
