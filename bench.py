@@ -162,6 +162,7 @@ def stage_bytes(pre):
     """Algorithmic HBM bytes of each apply stage."""
     nloc = pre.local_sizes
     loc = sum(8 * n * (kl + kv + 1) + 4 * n + 12 * n + 8 * n for n, (kl, kv) in zip(nloc, pre.local_bands))
+    loc += getattr(pre, "split_bytes", 0)  # split blocks: Sigma^-1, F and the spikes, read once
     zt = zy = asm = b0 = 0
     if pre.has_coarse:
         zt = sum(8 * n * m + 12 * n for n, m in pre.cblock_shapes)
@@ -185,6 +186,7 @@ def multi_stage_bytes(pre, nr):
     else:
         loc = sum(8 * n * (kl + kv + 1) + 4 * n + 4 * n for n, (kl, kv) in zip(nloc, pre.local_bands))
     loc += nr * sum(16 * n for n in nloc)  # gather r + write x_s per column
+    loc += getattr(pre, "split_bytes", 0)  # split blocks: Sigma^-1, F and the spikes, read once
     zt = zy = b0 = 0
     if pre.has_coarse:
         zt = sum(8 * n * m + 4 * n + 8 * n * nr for n, m in pre.cblock_shapes)

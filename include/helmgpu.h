@@ -61,7 +61,7 @@ extern "C" {
 #define HG_ERR_UNSUPPORTED 3
 #define HG_ERR_NOMEM 4
 
-#define HG_ABI_VERSION 3
+#define HG_ABI_VERSION 4
 
 /* Most right-hand sides one batched call handles (BASELINE config 5's
  * batch of 16 seeded load vectors). */
@@ -181,6 +181,48 @@ typedef struct {
   /* With b0_inv given: 0 = every apply uses it; 1 = only batched applies
    * (the single-RHS apply keeps the panel chain, which is shorter there). */
   int32_t b0_inv_batched_only;
+
+  /* Split local blocks (optional; n_split = 0: none).  A fine subdomain whose
+   * band solve is one long dependency chain (few, large blocks: config 5 at
+   * 8 x 8) may be given as P chunks of consecutive band rows separated by P-1
+   * separators of kl rows each (rows i < a and j >= a + kl of a band matrix
+   * do not couple).  Its local solve (ls.lu.solve, schwarz.py:58-60 — the same
+   * operator B_s^{-1}, eliminated in nested-dissection order) is then
+   *   y_p = A_p^{-1} r_p            every chunk: an ordinary local block above
+   *   x_S = Sigma^{-1} (r_S - F y)  Sigma = A_SS - sum_p F_p A_p^{-1} E_p
+   *   x_p = y_p - W_p x_S           W_p = A_p^{-1} E_p (the chunk's spikes)
+   * so the chain is 1/P as long and P times as many CTAs work.  Each chunk is
+   * a local block; the separators of split s are ONE pseudo block split_blk[s]
+   * with local_n = 0 whose index range (local_idx_off) lists the separator
+   * dofs (separator after separator).  Separator rows of all splits are
+   * numbered consecutively: split s owns rows split_row_off[s] ..
+   * split_row_off[s+1].  F (separator rows x chunk unknowns) is a CSR over
+   * those rows whose column entries are POSITIONS in the local solution
+   * scratch (local_idx_off[block] + row within the block).  Sigma^{-1} of
+   * split s is row-major nS x nS at split_sinv[split_sinv_off[s]].  Spike i
+   * belongs to chunk block spike_blk[i] of split spike_split[i]; it couples
+   * to separator rows spike_col0[i] .. + spike_w[i] of that split (spike_w a
+   * multiple of 8, zero padded) and is stored at spike_data[spike_off[i]] in
+   * 8 x 8 fragment blocks: block (mt, kb) at doubles (mt KB + kb) 64, element
+   * (lane = 4 g + q, h) at 2 lane + h = W[8 mt + g][8 kb + 4 h + q], rows
+   * zero padded to a multiple of 8 (KB = spike_w / 8). */
+  int32_t n_split;
+  const int32_t* split_blk;       /* n_split */
+  const int64_t* split_row_off;   /* n_split+1 */
+  const int64_t* split_f_indptr;  /* total separator rows + 1 */
+  const int64_t* split_f_pos;
+  const double* split_f_val;
+  const int64_t* split_sinv_off;  /* n_split, in doubles */
+  int64_t split_sinv_len;
+  const double* split_sinv;
+  int32_t n_spike;
+  const int32_t* spike_blk;       /* n_spike */
+  const int32_t* spike_split;
+  const int32_t* spike_col0;
+  const int32_t* spike_w;
+  const int64_t* spike_off;       /* n_spike, in doubles */
+  int64_t spike_len;
+  const double* spike_data;
 } HgPrecondDesc;
 
 /* ---- library ---- */

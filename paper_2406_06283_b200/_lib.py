@@ -71,6 +71,23 @@ class HgPrecondDesc(ctypes.Structure):
         ("factor_info", _i32p),
         ("factor_min_pivot", _f64p),
         ("b0_inv_batched_only", ctypes.c_int32),
+        ("n_split", ctypes.c_int32),
+        ("split_blk", _i32p),
+        ("split_row_off", _i64p),
+        ("split_f_indptr", _i64p),
+        ("split_f_pos", _i64p),
+        ("split_f_val", _f64p),
+        ("split_sinv_off", _i64p),
+        ("split_sinv_len", ctypes.c_int64),
+        ("split_sinv", _f64p),
+        ("n_spike", ctypes.c_int32),
+        ("spike_blk", _i32p),
+        ("spike_split", _i32p),
+        ("spike_col0", _i32p),
+        ("spike_w", _i32p),
+        ("spike_off", _i64p),
+        ("spike_len", ctypes.c_int64),
+        ("spike_data", _f64p),
     ]
 
 
@@ -137,7 +154,7 @@ SIGNATURES = {
 STAT_PANEL_ACTIVE, STAT_PANEL_DEVIATION, STAT_PANEL_BYTES = 1, 2, 3
 FIELD_LOCAL_FWD, FIELD_LOCAL_BWD = 1, 2
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 DEBUG_SPIN_LIMIT_MS, DEBUG_SKIP_ZT, DEBUG_FORCE_EXPLICIT_RHO = 1, 2, 3
 MAX_BASIS = 1024  # Krylov vectors the basis kernels support (MAX_NV)
 NPHASES = 7  # HG_NPHASES

@@ -782,6 +782,7 @@ int hg_precond_destroy(HgPrecond* P) {
   release(P->d_blk_done);
   release(P->d_y);
   release(P->d_b0_inv);
+  split_release(P);
   release(P->d_c);
   release(P->d_cm);
   release(P->d_ypart);
@@ -927,7 +928,9 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
     d.idx_off = D->local_idx_off[s];
     d.fwd_off = D->local_fwd_off[s];
     d.bwd_off = D->local_bwd_off[s];
-    if (d.n != D->local_idx_off[s + 1] - D->local_idx_off[s] || d.fstride < d.kl + 1 ||
+    // d.n = 0 with a non-empty index range: the separator pseudo block of a split subdomain
+    if ((d.n != D->local_idx_off[s + 1] - D->local_idx_off[s] && !(d.n == 0 && D->n_split > 0)) ||
+        d.fstride < d.kl + 1 ||
         d.bstride < d.kv + 1 || (d.fstride & 1) || (d.bstride & 1) || (d.fwd_off & 1) || (d.bwd_off & 1)) {
       set_error("hg_precond_create: inconsistent local block descriptor " + std::to_string(s));
       return HG_ERR_ARG;
@@ -966,6 +969,8 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
     HG_TRY(upload(&P->d_bwd, D->local_bwd, (size_t)D->local_bwd_len, bytes));
     if (!D->local_fwd || !D->local_bwd) HG_TRY(device_factor_local(P, D));
     HG_TRY(upload<double>(&P->d_xs, nullptr, (size_t)nidx, bytes));
+    HG_CUDA_TRY(cudaMemset(P->d_xs, 0, sizeof(double) * (size_t)nidx));
+    HG_TRY(split_upload(P, D));
     std::vector<int> ptr;
     std::vector<long long> ent;
     HG_TRY(build_contrib(n, D->n_local, D->local_idx_off, D->local_idx, ptr, ent));
@@ -1080,6 +1085,7 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
   HG_TRY(preload_dcgs2());
   HG_TRY(preload_add());
   HG_TRY(preload_b0_dense());
+  HG_TRY(preload_split());
   HG_CUDA_TRY(cudaStreamCreateWithFlags(&P->aux, cudaStreamNonBlocking));
   HG_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
   HG_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));

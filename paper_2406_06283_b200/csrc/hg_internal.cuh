@@ -30,6 +30,20 @@ struct CblkDesc {    // one coarse (Z) block
   long long part_off;  // into the Z^T r partials
 };
 
+struct SplitDesc {   // one split subdomain (helmgpu.h "Split local blocks")
+  long long row0;      // first of its rows in the global separator numbering
+  long long sep_pos;   // position of its separator unknowns in local_idx / the xs scratch
+  long long sinv_off;  // Sigma^{-1} (ns x ns row-major), doubles
+  int ns, pad;
+};
+
+struct SpikeDesc {   // spike block W_p of one chunk
+  long long pos;       // the chunk's position in the xs scratch
+  long long row0;      // first separator row of its split (global separator numbering)
+  long long off;       // packed data, doubles
+  int n, w, wtrue, col0;  // chunk rows; padded / true separator columns; first separator column
+};
+
 }  // namespace hg
 
 struct HgPrecond {
@@ -61,6 +75,19 @@ struct HgPrecond {
   // dof -> local contributions (positions in xs), fixed (subdomain) order
   int* d_lptr = nullptr;
   long long* d_lent = nullptr;
+
+  // split local blocks (hg_split.cu)
+  int n_split = 0, split_ns_max = 0, n_spike_items1 = 0, n_spike_items2 = 0;
+  hg::SplitDesc* d_split = nullptr;
+  long long* d_split_fptr = nullptr;
+  long long* d_split_fpos = nullptr;
+  double* d_split_fval = nullptr;
+  double* d_split_sinv = nullptr;
+  hg::SpikeDesc* d_spike = nullptr;
+  double* d_spike_data = nullptr;
+  int2* d_spike_items1 = nullptr;   // (spike, 8-row tile)
+  int2* d_spike_items2 = nullptr;   // (spike, pair of 8-row tiles)
+  double* d_xsep = nullptr;         // [separator row][HG_MAX_RHS] compact x_S
 
   // coarse part
   int m = 0;
@@ -234,6 +261,11 @@ int launch_b0_multi(HgPrecond* P, int nrhs, cudaStream_t st);
 int launch_b0_dense(HgPrecond* P, cudaStream_t st);
 int launch_b0_dense_multi(HgPrecond* P, int nrhs, cudaStream_t st);
 int preload_b0_dense();
+int split_upload(HgPrecond* P, const HgPrecondDesc* D);
+void split_release(HgPrecond* P);
+int launch_split_stages(HgPrecond* P, const double* R, long long ldr, double* xs, long long xs_len, int nrhs,
+                        cudaStream_t st);
+int preload_split();
 int pack_b0_inverse(int m, const double* d_binv, double** d_packed, int* mp_out);
 constexpr int B0_KSPLIT = 8;
 int launch_zy_multi(HgPrecond* P, int nrhs, cudaStream_t st);

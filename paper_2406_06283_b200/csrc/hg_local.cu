@@ -24,7 +24,8 @@ int preload_local(HgPrecond* P) {
 
 int launch_local_solve(HgPrecond* P, const double* r, cudaStream_t st) {
   if (P->n_local == 0) return HG_OK;
-  return launch_local_grid(P, P->d_local, P->n_local, r, st);
+  HG_TRY(launch_local_grid(P, P->d_local, P->n_local, r, st));
+  return launch_split_stages(P, r, 0, P->d_xs, 0, 1, st);  // split subdomains: separators, spikes
 }
 
 __global__ void k_scatter_local(int n, const int* __restrict__ idx, const double* __restrict__ src,

@@ -452,8 +452,11 @@ static int dev_upload(T** dptr, const T* host, size_t count, long long* bytes) {
 
 // batched local solves: panels when prepared and checked, else the row kernel
 int launch_local_batch(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st) {
-  if (P->panel_ok) return launch_local_panel(P, R, ldr, nrhs, st);
-  return launch_local_solve_multi(P, R, ldr, nrhs, st);
+  if (P->panel_ok)
+    HG_TRY(launch_local_panel(P, R, ldr, nrhs, st));
+  else
+    HG_TRY(launch_local_solve_multi(P, R, ldr, nrhs, st));
+  return launch_split_stages(P, R, ldr, P->d_xsm, P->xs_len, nrhs, st);  // split subdomains: separators, spikes
 }
 
 // ring stages: as many as fit beside the window with two CTAs per SM (at least

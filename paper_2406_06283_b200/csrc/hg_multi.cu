@@ -634,6 +634,7 @@ int multi_prepare(HgPrecond* P) {
     return HG_OK;
   };
   HG_TRY(alloc(&P->d_xsm, (size_t)MR * P->xs_len));
+  HG_CUDA_TRY(cudaMemset(P->d_xsm, 0, sizeof(double) * MR * P->xs_len));  // pseudo-block slots are read before written
   HG_TRY(alloc(&P->d_tmpm, (size_t)MR * P->n));
   if (P->m > 0) {
     HG_TRY(alloc(&P->d_zsm, (size_t)MR * P->zs_len));

@@ -26,7 +26,7 @@ import scipy.sparse as sp
 from . import _lib
 from .errors import SingularOperatorError
 from .factor import (BandLU, band_lu, block_bandwidth, lu_b0, pack_b0_tiles, pack_band_records, record_floor,
-                     record_widths, submatrix, swizzle_tile_rows, tile_span)
+                     record_widths, submatrix, swizzle_tile_rows, tile_span, pack_spike, split_block)
 
 _DENSE_EIG_LIMIT = 1500
 _SINGULAR_RTOL = 1e-12
@@ -106,16 +106,17 @@ class GpuBandLU:
     one block (hg_local_solve).  ``host`` = the host dgbtrf factors of the
     block (computed on first access when the device factorised it; tests)."""
 
-    def __init__(self, precond, index, host_factor):
+    def __init__(self, precond, index, host_factor, solver_index=None):
         self._p = precond
-        self._s = index
+        self._s = index  # device block
+        self._ls = index if solver_index is None else solver_index
         self._host = host_factor if isinstance(host_factor, BandLU) else None
         self.shape = (host_factor.n, host_factor.n)
 
     @property
     def host(self):
         if self._host is None:
-            ls = self._p.local_solvers[self._s]
+            ls = self._p.local_solvers[self._ls]
             self._host = band_lu(submatrix(self._p._B, ls.idof, ls.idof), label=(ls.coarse_index, ls.fine_index))
         return self._host
 
@@ -127,6 +128,53 @@ class GpuBandLU:
             _lib.load().hg_local_solve(self._p._handle, self._s, _vp(t), _vp(out), _stream()), "hg_local_solve"
         )
         return out.cpu().numpy() if was_np else out
+
+
+_SPLIT_G = {}
+
+
+def _split_worker(i):
+    a = _SPLIT_G["todo"][i]
+    if a is None:
+        return None
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(1):
+        return split_block(a[0], a[1], label=a[2])
+
+
+def _split_all(todo):
+    """factor.split_block of every entry, in a fork pool: the spikes are band
+    solves with kl or 2 kl right-hand sides per chunk (seconds per 18k-row
+    block).  Serial under a CUDA tool's injection (a fork crashes the tool)."""
+    from .problems import _tool_injected
+
+    workers = min(sum(a is not None for a in todo), os.cpu_count() or 1)
+    if workers <= 1 or _tool_injected() or os.environ.get("HG_SPLIT_WORKERS") == "1":
+        return [split_block(a[0], a[1], label=a[2]) if a is not None else None for a in todo]
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+
+    _SPLIT_G["todo"] = todo
+    try:
+        with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("fork")) as ex:
+            return list(ex.map(_split_worker, range(len(todo))))
+    finally:
+        _SPLIT_G.clear()
+
+
+class SplitLocalLU:
+    """``LocalSolver.lu`` of a subdomain whose block is split into chunks and
+    separators (factor.split_block): its solve exists only inside the
+    preconditioner apply (chunk solves, separator system and spike update are
+    three device stages over all subdomains at once)."""
+
+    def __init__(self, n):
+        self.shape = (n, n)
+
+    def solve(self, rhs):
+        raise NotImplementedError("this subdomain's block is split (HG_LOCAL_SPLIT); its local solve runs inside "
+                                  "apply() / apply_multi()")
 
 
 class LocalSolver:
@@ -256,17 +304,41 @@ class TwoLevelPreconditioner:
             self.local_solvers.append(LocalSolver(i, j, idof, None, getattr(sub, "diameter", np.nan), block,
                                                   matrix=B))
         bws = [block_bandwidth(b) if b.shape[0] else 0 for b in blocks]
+        nsplit = self._split_chunks(blocks, bws)
         self.device_factor = (os.environ.get("HG_HOST_FACTOR", "0") != "1" and not self._host_only_factor()
-                              and max(bws, default=0) <= DEVICE_BAND_MAX)
-        for ls, block, bw in zip(self.local_solvers, blocks, bws):
+                              and max(bws, default=0) <= DEVICE_BAND_MAX and nsplit < 2)
+        # device blocks: one per subdomain, or (split subdomains) its chunks followed by a pseudo
+        # block of the separator dofs (factor.split_block; include/helmgpu.h "Split local blocks")
+        self.splits = []          # (subdomain index, SplitBlock, first device block)
+        self._dev_block = []      # subdomain -> device block (None when split)
+        self._dev_labels = []
+        split_of = {}
+        if nsplit >= 2:
+            todo = [(b, nsplit, (ls.coarse_index, ls.fine_index)) if b.shape[0] else None
+                    for ls, b in zip(self.local_solvers, blocks)]
+            split_of = dict(enumerate(_split_all(todo)))
+        for s, (ls, block, bw) in enumerate(zip(self.local_solvers, blocks, bws)):
+            label = (ls.coarse_index, ls.fine_index)
+            sb = split_of.get(s)
+            if sb is not None:
+                self.splits.append((s, sb, len(factors)))
+                self._dev_block.append(None)
+                for rows, f in sb.chunks:
+                    factors.append((ls.idof[rows], f))
+                    self._dev_labels.append(label)
+                factors.append((ls.idof[sb.sep_rows], band_lu(sp.csr_matrix((0, 0)))))
+                self._dev_labels.append(label)
+                continue
             if self.device_factor:
                 f = types.SimpleNamespace(n=block.shape[0], kl=bw, ku=bw, kv=2 * bw, block=block,
                                           norm=float(np.sqrt(np.sum(block.data ** 2))) if block.nnz else 0.0)
             elif block.shape[0]:
-                f = band_lu(block, label=(ls.coarse_index, ls.fine_index))
+                f = band_lu(block, label=label)
             else:
                 f = band_lu(sp.csr_matrix((0, 0)))
+            self._dev_block.append(len(factors))
             factors.append((ls.idof, f))
+            self._dev_labels.append(label)
         self.setup_times["local_blocks"] = self._t() - t0
 
         # ---- coarse operator (schwarz.py:87-100)
@@ -282,7 +354,21 @@ class TwoLevelPreconditioner:
             cblocks = coarse_blocks(coarse, dec)
         self._upload(B, Dk, factors, cblocks, lu, piv)
         for s, ls in enumerate(self.local_solvers):
-            ls.lu = GpuBandLU(self, s, factors[s][1])
+            b = self._dev_block[s]
+            ls.lu = GpuBandLU(self, b, factors[b][1], s) if b is not None else SplitLocalLU(ls.idof.size)
+
+    @staticmethod
+    def _split_chunks(blocks, bws):
+        """Chunks per subdomain for the split local solve (1 = none).  HG_LOCAL_SPLIT = P forces it;
+        the default splits only decompositions with fewer blocks than half the SMs and wide bands
+        (config 5 at 8 x 8: 64 blocks of 18k rows, kl = 136) in two."""
+        env = os.environ.get("HG_LOCAL_SPLIT", "auto")
+        if env != "auto":
+            return max(1, int(env))
+        nb = sum(1 for b in blocks if b.shape[0])
+        if nb == 0 or nb > 74 or max(bws, default=0) < 96:
+            return 1
+        return 2  # measured at 5-8: 2 chunks (128 chains, one wave) beat 4 and 8 (more spike bytes, same wave count)
 
     def _host_only_factor(self):
         return getattr(self, "_host_only", False)  # host_image(): no device to factor on
@@ -290,7 +376,7 @@ class TwoLevelPreconditioner:
     # ------------------------------------------------------------------ upload
     def _upload(self, B, Dk, factors, cblocks, lu, piv):
         arrays, meta = self._image(B, Dk, factors, cblocks, lu, piv)
-        meta["labels"] = [[int(ls.coarse_index), int(ls.fine_index)] for ls in self.local_solvers]
+        meta["labels"] = [[int(a), int(b)] for a, b in self._dev_labels]
         if getattr(self, "_host_only", False):
             self._image_arrays, self._meta = arrays, meta
             return
@@ -365,7 +451,10 @@ class TwoLevelPreconditioner:
             idof = np.asarray(idx[off[s]:off[s + 1]], dtype=np.int64)
             kl, kv = meta["local_bands"][s]
             ls = LocalSolver(ci, fi, idof, None, np.nan, None, matrix=self._B)
-            ls.lu = GpuBandLU(self, s, types.SimpleNamespace(n=int(idof.size), kl=kl, kv=kv))
+            if idof.size and int(arrays["local_n"][s]) == 0:  # separator pseudo block of a split subdomain
+                ls.lu = SplitLocalLU(int(idof.size))
+            else:
+                ls.lu = GpuBandLU(self, s, types.SimpleNamespace(n=int(idof.size), kl=kl, kv=kv))
             self.local_solvers.append(ls)
         return self
 
@@ -447,6 +536,7 @@ class TwoLevelPreconditioner:
             put("local_fwd", np.concatenate(fwd_parts) if fwd_parts else np.zeros(0), f64)
             put("local_bwd", np.concatenate(bwd_parts) if bwd_parts else np.zeros(0), f64)
         M["local_bands"] = [[int(f.kl), int(f.kv)] for _, f in factors]
+        self._image_splits(A, M, idx_off)
 
         m = sum(b.shape[1] for _, b in cblocks)
         M["m"] = int(m)
@@ -535,6 +625,69 @@ class TwoLevelPreconditioner:
             put("b0_tiles", tiles, f64)
         return A, M
 
+    def _image_splits(self, A, M, idx_off):
+        """Descriptor arrays of the split local blocks (helmgpu.h "Split local blocks")."""
+        i32, i64, f64 = np.int32, np.int64, np.float64
+        splits = getattr(self, "splits", [])
+        M["n_split"] = len(splits)
+        M["n_spike"] = 0
+        M["split_sinv_len"] = M["spike_len"] = 0
+        M["split_bytes"] = 0
+        if not splits:
+            return
+        blk, row_off, fptr, fpos, fval, soff, sinv = [], [0], [0], [], [], [], []
+        kblk, ksplit, kcol0, kw, koff, kdata = [], [], [], [], [], []
+        spos = kpos = 0
+        for si, (s, sb, b0) in enumerate(splits):
+            nchunk = len(sb.chunks)
+            blk.append(b0 + nchunk)
+            row_off.append(row_off[-1] + sb.sep_rows.size)
+            # block-local row -> position in the local solution scratch
+            pos = np.full(sb.F.shape[1], -1, dtype=np.int64)
+            for p, (rows, _) in enumerate(sb.chunks):
+                pos[rows] = idx_off[b0 + p] + np.arange(rows.size)
+            F = sp.csr_matrix(sb.F)
+            F.sort_indices()
+            if (pos[F.indices] < 0).any():
+                raise ValueError("separator rows couple to a non-chunk column")
+            fptr.extend((fptr[-1] + F.indptr[1:]).tolist())
+            fpos.append(pos[F.indices])
+            fval.append(F.data)
+            soff.append(spos)
+            sinv.append(sb.sinv.ravel())
+            spos += sb.sinv.size
+            for p, (c0, w, W) in enumerate(sb.spikes):
+                if w == 0:
+                    continue
+                pk = pack_spike(W)
+                kblk.append(b0 + p)
+                ksplit.append(si)
+                kcol0.append(c0)
+                kw.append(w)
+                koff.append(kpos)
+                kdata.append(pk)
+                kpos += pk.size
+        A["split_blk"] = np.ascontiguousarray(blk, dtype=i32)
+        A["split_row_off"] = np.ascontiguousarray(row_off, dtype=i64)
+        A["split_f_indptr"] = np.ascontiguousarray(fptr, dtype=i64)
+        A["split_f_pos"] = np.ascontiguousarray(np.concatenate(fpos), dtype=i64)
+        A["split_f_val"] = np.ascontiguousarray(np.concatenate(fval), dtype=f64)
+        A["split_sinv_off"] = np.ascontiguousarray(soff, dtype=i64)
+        A["split_sinv"] = np.ascontiguousarray(np.concatenate(sinv), dtype=f64)
+        M["split_sinv_len"] = int(spos)
+        M["n_spike"] = len(kblk)
+        A["spike_blk"] = np.ascontiguousarray(kblk, dtype=i32)
+        A["spike_split"] = np.ascontiguousarray(ksplit, dtype=i32)
+        A["spike_col0"] = np.ascontiguousarray(kcol0, dtype=i32)
+        A["spike_w"] = np.ascontiguousarray(kw, dtype=i32)
+        A["spike_off"] = np.ascontiguousarray(koff, dtype=i64)
+        A["spike_data"] = np.ascontiguousarray(np.concatenate(kdata), dtype=f64)
+        M["spike_len"] = int(kpos)
+        # bytes one local solve reads beyond the chunk records: Sigma^{-1}, F, the spikes
+        M["split_bytes"] = int(8 * spos + 16 * A["split_f_pos"].size + 8 * kpos)
+        M["split_chunks"] = int(max(len(sb.chunks) for _, sb, _ in splits))
+        M["split_cond"] = float(max(sb.cond for _, sb, _ in splits))
+
     def _getrs(self):
         """c -> getrs(lu, piv, c) (the reference's lu_solve, schwarz.py:56) with the
         same getrf factors; on the device when there is one (the factors are
@@ -617,6 +770,8 @@ class TwoLevelPreconditioner:
         self.b0_dense = bool(meta["b0_dense"])
         self.b0_dense_dev = meta.get("b0_dense_dev")
         self.b0_tile_dev = meta.get("b0_tile_dev")
+        self.split_bytes = int(meta.get("split_bytes", 0))
+        self.n_split = int(meta.get("n_split", 0))
         self.panel_active = bool(lib.hg_precond_stat(h, _lib.STAT_PANEL_ACTIVE) == 1.0)
         self.panel_deviation = float(lib.hg_precond_stat(h, _lib.STAT_PANEL_DEVIATION))
         # factor bytes one batched local solve streams (16-row panel records, hg_local_panel.cu)

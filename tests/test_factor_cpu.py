@@ -91,3 +91,82 @@ def test_record_floor_padding():
     r = rng.standard_normal(n)
     got = emulate_band_records(fwd.reshape(n, fs), bwd.reshape(n, bs), n, klp, kvp, r)
     assert np.abs(got - f.solve(r)).max() <= 1e-12 * np.abs(f.solve(r)).max()
+
+
+def test_split_block_is_the_same_local_operator():
+    """factor.split_block (chunks + separators + spikes) against dgbtrs of the
+    whole block, and the descriptor arrays the device consumes (helmgpu.h
+    "Split local blocks") interpreted exactly as hg_split.cu does."""
+    import os
+
+    import paper_2406_06283_b200 as hg
+    from paper_2406_06283_b200 import factor, schwarz
+    from _helpers import emulate_band_records
+
+    P = hg.build_problem("1", workers=1, one_level=True)
+    B = P.forms.helmholtz.tocsr()
+    subs = [np.asarray(sub.idof) for _, _, sub in P.dec.fine_flat()]
+    rng = np.random.default_rng(2)
+    blk = factor.submatrix(B, subs[5], subs[5])
+    whole = factor.band_lu(blk)
+    r = rng.standard_normal(blk.shape[0])
+    for nchunk in (2, 3):
+        sb = factor.split_block(blk, nchunk)
+        assert len(sb.chunks) == nchunk and sb.sep_rows.size == (nchunk - 1) * whole.kl
+        assert np.abs(sb.solve(r) - whole.solve(r)).max() <= 1e-12 * np.abs(whole.solve(r)).max()
+    assert factor.split_block(blk, 6) is None  # chunks shorter than four band widths: declined
+
+    old = os.environ.get("HG_LOCAL_SPLIT")
+    os.environ["HG_LOCAL_SPLIT"] = "2"
+    try:
+        A, M = schwarz.host_image(P.forms, P.dec, None)
+    finally:
+        if old is None:
+            del os.environ["HG_LOCAL_SPLIT"]
+        else:
+            os.environ["HG_LOCAL_SPLIT"] = old
+    assert M["n_split"] == len(subs) and M["n_local"] == 3 * len(subs)
+    rg = rng.standard_normal(B.shape[0])
+    xs = np.zeros(int(A["local_idx_off"][-1]))
+    off, idx = A["local_idx_off"], A["local_idx"]
+    for b in range(M["n_local"]):  # chunk solves from the packed records
+        n = int(A["local_n"][b])
+        if n == 0:
+            continue
+        fs, bs = int(A["local_fstride"][b]), int(A["local_bstride"][b])
+        fw = A["local_fwd"][A["local_fwd_off"][b]:A["local_fwd_off"][b] + n * fs].reshape(n, fs)
+        bw = A["local_bwd"][A["local_bwd_off"][b]:A["local_bwd_off"][b] + n * bs].reshape(n, bs)
+        xs[off[b]:off[b] + n] = emulate_band_records(fw, bw, n, int(A["local_kl"][b]), int(A["local_kv"][b]),
+                                                    rg[idx[off[b]:off[b] + n]])
+    xsep = np.zeros(int(A["split_row_off"][-1]))
+    for s in range(M["n_split"]):  # separators
+        r0, r1 = int(A["split_row_off"][s]), int(A["split_row_off"][s + 1])
+        pb = int(A["split_blk"][s])
+        t = rg[idx[off[pb]:off[pb + 1]]].copy()
+        for k in range(r1 - r0):
+            a, e = int(A["split_f_indptr"][r0 + k]), int(A["split_f_indptr"][r0 + k + 1])
+            t[k] -= A["split_f_val"][a:e] @ xs[A["split_f_pos"][a:e]]
+        ns = r1 - r0
+        so = int(A["split_sinv_off"][s])
+        xsep[r0:r1] = A["split_sinv"][so:so + ns * ns].reshape(ns, ns) @ t
+        xs[off[pb]:off[pb] + ns] = xsep[r0:r1]
+    for i in range(M["n_spike"]):  # spikes, from the packed fragment blocks
+        b, s = int(A["spike_blk"][i]), int(A["spike_split"][i])
+        n, w, c0 = int(A["local_n"][b]), int(A["spike_w"][i]), int(A["spike_col0"][i])
+        mt = (n + 7) // 8
+        pk = A["spike_data"][A["spike_off"][i]:A["spike_off"][i] + mt * 8 * w].reshape(mt, w // 8, 8, 4, 2)
+        W = pk.transpose(0, 2, 1, 4, 3).reshape(mt * 8, w)[:n]  # (mt, g, kb, h, q)
+        r0 = int(A["split_row_off"][s])
+        ns = int(A["split_row_off"][s + 1]) - r0
+        xv = np.zeros(w)
+        k = min(w, ns - c0)
+        xv[:k] = xsep[r0 + c0:r0 + c0 + k]
+        xs[off[b]:off[b] + n] -= W @ xv
+    # assemble in block order and compare with the sum of whole-block solves
+    got = np.zeros(B.shape[0])
+    for b in range(M["n_local"]):
+        np.add.at(got, idx[off[b]:off[b + 1]], xs[off[b]:off[b + 1]])
+    want = np.zeros(B.shape[0])
+    for idof in subs:
+        want[idof] += factor.band_lu(factor.submatrix(B, idof, idof)).solve(rg[idof])
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
