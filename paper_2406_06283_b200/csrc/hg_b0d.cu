@@ -120,8 +120,11 @@ int launch_b0_dense(HgPrecond* P, cudaStream_t st) {
   return HG_OK;
 }
 
+// C in DMMA B-fragment order: k-step (kb, h) = rows 8 kb + 4 h + q of C; lane (g, q) holds
+// {C[row][g], C[row][8 + g]} as one double2 at ((2 kb + h) 32 + lane) — one 16-byte load per lane
+// per k-step in the GEMM, 512 contiguous bytes per warp
 __global__ void k_creduce_multi(int m, int nrhs, const int* __restrict__ col_blk, const CblkDesc* __restrict__ descs,
-                                const double* __restrict__ cpartm, double* __restrict__ C) {
+                                const double* __restrict__ cpartm, double* __restrict__ Cf) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   const int i = e / MRD, col = e % MRD;
   if (i >= m) return;
@@ -131,13 +134,14 @@ __global__ void k_creduce_multi(int m, int nrhs, const int* __restrict__ col_blk
     const int l = i - d.col0;
     for (int ch = 0; ch < d.nchunk; ++ch) v += cpartm[(d.part_off + (long long)ch * d.m + l) * MRD + col];
   }
-  C[e] = v;
+  const int kb = i >> 3, h = (i >> 2) & 1, q = i & 3, g = col & 7, nt = col >> 3;
+  Cf[(((size_t)(kb * 2 + h) * 32 + g * 4 + q) << 1) + nt] = v;
 }
 
 // Y_slice[s][rows of this warp] = B0^{-1}[rows, k in slice s] C[k in slice s, :]: a warp owns two 8-row
 // tiles (4 DMMA accumulators for the 16 columns), streams their packed fragments and takes the B
-// fragments of C (mp x 16, zero padded; 2 MB, L1 / L2 resident) straight from global memory — no
-// shared memory, no barrier.
+// fragments of C (fragment order, zero padded; 2 MB, L1 / L2 resident) straight from global memory —
+// no shared memory, no barrier.
 __global__ void __launch_bounds__(256) k_b0_gemm_multi(int mp, const double2* __restrict__ Bpk,
                                                        const double* __restrict__ C, double* __restrict__ Yp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, g = lane >> 2;
@@ -150,7 +154,7 @@ __global__ void __launch_bounds__(256) k_b0_gemm_multi(int mp, const double2* __
   const int ka = slice * kbl, kb = min(KB, ka + kbl);
   const double2* a0p = Bpk + ((size_t)mt0 * KB + ka) * 32 + lane;
   const double2* a1p = two ? a0p + (size_t)KB * 32 : a0p;
-  const double* cp = C + ((size_t)ka * 8 + q) * MRD + g;
+  const double2* cp = reinterpret_cast<const double2*>(C) + (size_t)ka * 64 + lane;
   double acc[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
   // register double buffer: the A fragments of the next GU k-blocks are in flight while the
   // current GU are multiplied (2 GU 512-byte loads per warp ahead of their use)
@@ -179,16 +183,16 @@ __global__ void __launch_bounds__(256) k_b0_gemm_multi(int mp, const double2* __
 #pragma unroll
     for (int u = 0; u < GU; ++u) {
       if (k + u < kb) {
-        const double* cu = cp + (size_t)(k - ka + u) * 8 * MRD;
-        const double b00 = __ldg(cu), b01 = __ldg(cu + 8), b10 = __ldg(cu + 4 * MRD), b11 = __ldg(cu + 4 * MRD + 8);
-        dmma_d(acc[0][0], c0[u].x, b00);
-        dmma_d(acc[0][1], c0[u].x, b01);
-        dmma_d(acc[1][0], c1[u].x, b00);
-        dmma_d(acc[1][1], c1[u].x, b01);
-        dmma_d(acc[0][0], c0[u].y, b10);
-        dmma_d(acc[0][1], c0[u].y, b11);
-        dmma_d(acc[1][0], c1[u].y, b10);
-        dmma_d(acc[1][1], c1[u].y, b11);
+        const double2* cu = cp + (size_t)(k - ka + u) * 64;
+        const double2 b0 = __ldg(cu), b1 = __ldg(cu + 32);
+        dmma_d(acc[0][0], c0[u].x, b0.x);
+        dmma_d(acc[0][1], c0[u].x, b0.y);
+        dmma_d(acc[1][0], c1[u].x, b0.x);
+        dmma_d(acc[1][1], c1[u].x, b0.y);
+        dmma_d(acc[0][0], c0[u].y, b1.x);
+        dmma_d(acc[0][1], c0[u].y, b1.y);
+        dmma_d(acc[1][0], c1[u].y, b1.x);
+        dmma_d(acc[1][1], c1[u].y, b1.y);
       }
     }
   }

@@ -479,15 +479,18 @@ static size_t panel_smem(const HgPrecond* P) {
 int launch_local_panel(HgPrecond* P, const double* R, long long ldr, int nrhs, cudaStream_t st) {
   if (P->n_local == 0) return HG_OK;
   const size_t smem = panel_smem(P);
-  // column split: two CTAs per block (8 columns each) while that still leaves every CTA resident
-  // (2 per SM); HG_PANEL_CSPLIT=0/1 overrides
+  // column split: two CTAs per block (8 columns each) while every CTA still has an SM to itself
+  // (measured: two column-split CTAs sharing an SM are slower than one 16-column CTA);
+  // HG_PANEL_CSPLIT=0/1 overrides
   static const int env = getenv("HG_PANEL_CSPLIT") ? atoi(getenv("HG_PANEL_CSPLIT")) : -1;
   int sms = 148;
   {
     int dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const bool split = nrhs > 8 && (env >= 0 ? env != 0 : 2 * P->n_local <= 2 * sms);
+  int nblk = 0;  // blocks with rows (separator pseudo blocks of split subdomains have none)
+  for (const LocalDesc& d : P->h_local) nblk += d.n > 0;
+  const bool split = nrhs > 8 && (env >= 0 ? env != 0 : 2 * nblk <= sms);
   const void* fn = split ? reinterpret_cast<const void*>(k_local_panel<1>)
                          : reinterpret_cast<const void*>(k_local_panel<2>);
   HG_TRY(ensure_func_attrs(fn, smem, false));

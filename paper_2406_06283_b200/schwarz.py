@@ -133,6 +133,29 @@ class GpuBandLU:
 _SPLIT_G = {}
 
 
+def _split_one(block, nchunk, label):
+    """factor.split_block with its guard: the split solve must be backward
+    stable on the whole block (normwise backward error of two seeded solves
+    <= 1e-13; a stable solver sits near 1e-16).  A chunk that is itself
+    (numerically) singular — k^2 at a Dirichlet eigenvalue of the chunk, not
+    of the block — or a failed guard leaves the subdomain unsplit."""
+    try:
+        sb = split_block(block, nchunk, label=label)
+    except SingularOperatorError:
+        return None
+    if sb is None:
+        return None
+    rng = np.random.default_rng(2406)
+    anorm = abs(block).sum(axis=1).max()
+    for _ in range(2):
+        r = rng.standard_normal(block.shape[0])
+        x = sb.solve(r)
+        eta = np.abs(r - block @ x).max() / (anorm * np.abs(x).max() + np.abs(r).max())
+        if not eta <= 1e-13:
+            return None
+    return sb
+
+
 def _split_worker(i):
     a = _SPLIT_G["todo"][i]
     if a is None:
@@ -140,7 +163,7 @@ def _split_worker(i):
     from threadpoolctl import threadpool_limits
 
     with threadpool_limits(1):
-        return split_block(a[0], a[1], label=a[2])
+        return _split_one(*a)
 
 
 def _split_all(todo):
@@ -151,7 +174,7 @@ def _split_all(todo):
 
     workers = min(sum(a is not None for a in todo), os.cpu_count() or 1)
     if workers <= 1 or _tool_injected() or os.environ.get("HG_SPLIT_WORKERS") == "1":
-        return [split_block(a[0], a[1], label=a[2]) if a is not None else None for a in todo]
+        return [_split_one(*a) if a is not None else None for a in todo]
     import multiprocessing as mp
     from concurrent.futures import ProcessPoolExecutor
 
