@@ -465,7 +465,8 @@ def run_ours(args, dist):
     # ---------------- e2e through the C ABI with host buffers
     e2e = None
     if not args.no_e2e:
-        Fh = torch.from_numpy(np.ascontiguousarray(rhs_host)).pin_memory().numpy()
+        # pinned, column-major (n, nrhs): the layout the C ABI takes (column c at F + c n)
+        Fh = torch.from_numpy(np.ascontiguousarray(rhs_host.T)).pin_memory().numpy().T
         pre.solve_host_batch(Fh, rtol=rtol, maxit=maxit)
         torch.cuda.synchronize()
         dist.barrier()

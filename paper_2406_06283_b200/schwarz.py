@@ -932,7 +932,9 @@ class TwoLevelPreconditioner:
         nrhs = F.shape[1]
         if not 1 <= nrhs <= _lib.MAX_RHS:
             raise ValueError("batch of %d columns; 1..%d supported per call" % (nrhs, _lib.MAX_RHS))
-        Fc = np.ascontiguousarray(F.T)
+        # the C ABI takes column c at F + c n: a column-major (Fortran-ordered) F is passed as it is,
+        # a row-major one is transposed on the host first (a strided 8 n nrhs-byte copy)
+        Fc = F.T if F.T.flags.c_contiguous else np.ascontiguousarray(F.T)
         Xc = np.empty_like(Fc)
         maxit = int(min(maxit, self.n))
         hist = np.zeros((nrhs, maxit + 1))
@@ -944,7 +946,7 @@ class TwoLevelPreconditioner:
             ),
             "hg_solve_host_batch",
         )
-        return Xc.T.copy(), _reports(hist, info, None)
+        return Xc.T, _reports(hist, info, None)  # (n, nrhs), column-major: no host transpose
 
     def close(self):
         if self._handle is not None:
