@@ -792,6 +792,11 @@ int hg_precond_destroy(HgPrecond* P) {
   release(P->d_tmp);
   release(P->d_xsm);
   release(P->d_zsm);
+  release(P->d_zypk);
+  release(P->d_ztpk);
+  release(P->d_zypk_off);
+  release(P->d_ztpk_off);
+  release(P->d_zy_items);
   release(P->d_cpartm);
   release(P->d_ym);
   release(P->d_b0m_x);

@@ -145,6 +145,13 @@ struct HgPrecond {
   double* d_zsm = nullptr;        // [c][zs_len] Z_b Y_b rows
   double* d_cpartm = nullptr;     // [part_len][HG_MAX_RHS] Z^T R partials
   double* d_ym = nullptr;         // [m][HG_MAX_RHS] coarse solution
+  // packed copies of Z for the batched contractions (hg_multi.cu "packed Z")
+  double* d_zypk = nullptr;
+  double* d_ztpk = nullptr;
+  long long* d_zypk_off = nullptr;
+  long long* d_ztpk_off = nullptr;
+  int2* d_zy_items = nullptr;     // (block, pair of 8-row tiles)
+  int n_zy_items = 0;
   double* d_b0m_x = nullptr;      // [2][K*64][HG_MAX_RHS] phase solutions
   double* d_tmpm = nullptr;       // [c][n] scratch (B U for the batched apply_T)
   cudaStream_t aux = nullptr;     // coarse chain runs here, forked/joined per apply

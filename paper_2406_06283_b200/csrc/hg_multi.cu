@@ -121,6 +121,10 @@ int launch_spmm_self(const DevCsr& A, const double* vals, const double* X, long 
 }
 
 // ------------------------------------------------------------------ Z^T R
+__global__ void k_zt_multi_pk(const int2*, const CblkDesc*, const int*, const long long*, const double2*, const double*,
+                              long long, int, double*, unsigned long long*);
+__global__ void k_zy_multi_pk(const int2*, int, const CblkDesc*, const long long*, const double2*, const double*, int,
+                              double*, long long);
 __global__ void __launch_bounds__(256) k_zt_multi(const int2* __restrict__ items, const CblkDesc* __restrict__ descs,
                                                   const int* __restrict__ idx, const double* __restrict__ Z,
                                                   const double* __restrict__ R, long long ldr, int nrhs,
@@ -169,8 +173,13 @@ int launch_zt_multi(HgPrecond* P, const double* R, long long ldr, int nrhs, cuda
     --P->skip_zt;
     return HG_OK;
   }
-  k_zt_multi<<<P->n_zt_items, 256, 0, st>>>(P->d_zt_items, P->d_cblk, P->d_cblk_idx, P->d_z, R, ldr, nrhs,
-                                             P->d_cpartm, P->d_blkm_done);
+  if (P->d_ztpk)
+    k_zt_multi_pk<<<P->n_zt_items, 256, 0, st>>>(P->d_zt_items, P->d_cblk, P->d_cblk_idx, P->d_ztpk_off,
+                                                  reinterpret_cast<const double2*>(P->d_ztpk), R, ldr, nrhs,
+                                                  P->d_cpartm, P->d_blkm_done);
+  else
+    k_zt_multi<<<P->n_zt_items, 256, 0, st>>>(P->d_zt_items, P->d_cblk, P->d_cblk_idx, P->d_z, R, ldr, nrhs,
+                                               P->d_cpartm, P->d_blkm_done);
   HG_LAUNCH_CHECK();
   return HG_OK;
 }
@@ -227,9 +236,170 @@ __global__ void __launch_bounds__(256) k_zy_multi(const int2* __restrict__ items
 
 int launch_zy_multi(HgPrecond* P, int nrhs, cudaStream_t st) {
   if (P->m == 0 || P->n_zt_items == 0) return HG_OK;
-  k_zy_multi<<<P->n_zt_items, 256, 0, st>>>(P->d_zt_items, P->d_cblk, P->d_z, P->d_ym, nrhs, P->d_zsm, P->zs_len);
+  if (P->d_zypk)
+    k_zy_multi_pk<<<ceil_div(P->n_zy_items, 8), 256, 0, st>>>(P->d_zy_items, P->n_zy_items, P->d_cblk, P->d_zypk_off,
+                                                               reinterpret_cast<const double2*>(P->d_zypk), P->d_ym,
+                                                               nrhs, P->d_zsm, P->zs_len);
+  else
+    k_zy_multi<<<P->n_zt_items, 256, 0, st>>>(P->d_zt_items, P->d_cblk, P->d_z, P->d_ym, nrhs, P->d_zsm, P->zs_len);
   HG_LAUNCH_CHECK();
   return HG_OK;
+}
+
+// ------------------------------------------------------------------ packed Z (batched applies)
+// The batched contractions stream Z in DMMA A-fragment order (8 x 8 blocks, one 16-byte load per
+// lane per two k-steps, 512 contiguous bytes per warp load — as B0^{-1} in hg_b0d.cu), built once
+// from the row-major blocks on the first batched call:
+//   zy copy: block b, row tile mt, k-block kb (coarse columns 8 kb ..) at double2 index
+//            zoff[b] / 2 + (mt KB_b + kb) 32 + lane: {Z[8 mt + g][8 kb + q], Z[8 mt + g][8 kb + 4 + q]}
+//   zt copy: block b, 256-row chunk ch, coarse-column tile mt, k-block kb (rows 256 ch + 8 kb ..):
+//            toff[b] / 2 + ((ch MT_b + mt) 32 + kb) 32 + lane:
+//            {Z[r0 + 8 kb + q][8 mt + g], Z[r0 + 8 kb + 4 + q][8 mt + g]}     (A = Z^T)
+// both zero padded to whole tiles.
+__global__ void k_zpack_zy(const CblkDesc* __restrict__ descs, const long long* __restrict__ zoff,
+                           const double* __restrict__ Z, double2* __restrict__ out) {
+  const CblkDesc d = descs[blockIdx.y];
+  const int KB = (d.m + 7) >> 3, MT = (d.n + 7) >> 3;
+  const long long ne = (long long)MT * KB * 32;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (long long)gridDim.x * blockDim.x) {
+    const int lane = (int)(e & 31), g = lane >> 2, q = lane & 3;
+    const long long blk = e >> 5;
+    const int kb = (int)(blk % KB), mt = (int)(blk / KB);
+    const int row = mt * 8 + g, c0 = kb * 8 + q, c1 = c0 + 4;
+    double2 v;
+    v.x = (row < d.n && c0 < d.m) ? Z[d.z_off + (long long)row * d.m + c0] : 0.0;
+    v.y = (row < d.n && c1 < d.m) ? Z[d.z_off + (long long)row * d.m + c1] : 0.0;
+    out[(zoff[blockIdx.y] >> 1) + e] = v;
+  }
+}
+
+__global__ void k_zpack_zt(const CblkDesc* __restrict__ descs, const long long* __restrict__ toff,
+                           const double* __restrict__ Z, double2* __restrict__ out) {
+  const CblkDesc d = descs[blockIdx.y];
+  const int MT = (d.m + 7) >> 3;
+  const long long ne = (long long)d.nchunk * MT * 32 * 32;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (long long)gridDim.x * blockDim.x) {
+    const int lane = (int)(e & 31), g = lane >> 2, q = lane & 3;
+    long long t = e >> 5;
+    const int kb = (int)(t & 31);
+    t >>= 5;
+    const int mt = (int)(t % MT), ch = (int)(t / MT);
+    const int col = mt * 8 + g, r0 = ch * ZROWS + kb * 8 + q, r1 = r0 + 4;
+    double2 v;
+    v.x = (col < d.m && r0 < d.n) ? Z[d.z_off + (long long)r0 * d.m + col] : 0.0;
+    v.y = (col < d.m && r1 < d.n) ? Z[d.z_off + (long long)r1 * d.m + col] : 0.0;
+    out[(toff[blockIdx.y] >> 1) + e] = v;
+  }
+}
+
+// C_b partial of one (block, 256-row chunk): the gathered chunk of R in shared memory (B
+// fragments), a warp per 8-column tile of the block streaming its packed Z^T fragments
+__global__ void __launch_bounds__(256) k_zt_multi_pk(const int2* __restrict__ items, const CblkDesc* __restrict__ descs,
+                                                     const int* __restrict__ idx, const long long* __restrict__ toff,
+                                                     const double2* __restrict__ zt, const double* __restrict__ R,
+                                                     long long ldr, int nrhs, double* __restrict__ cpartm,
+                                                     unsigned long long* __restrict__ blk_done) {
+  __shared__ __align__(16) double s_r[ZROWS * SR];
+  const int2 it = items[blockIdx.x];
+  const CblkDesc d = descs[it.x];
+  const int k0 = it.y * ZROWS, rows = min(ZROWS, d.n - k0);
+  const int* ib = idx + d.idx_off + k0;
+  for (int e = threadIdx.x; e < ZROWS * MR; e += 256) {  // gather the chunk, zero padded
+    const int k = e % ZROWS, c = e / ZROWS;
+    double v = 0.0;
+    if (k < rows && c < nrhs) v = __ldg(R + (long long)c * ldr + __ldg(ib + k));
+    s_r[k * SR + c] = v;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, g = lane >> 2;
+  const int MT = (d.m + 7) >> 3;
+  const double2* base = zt + (toff[it.x] >> 1) + (size_t)it.y * MT * 1024;
+  for (int mt = warp; mt < MT; mt += 8) {
+    const double2* ap = base + (size_t)mt * 1024 + lane;
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+#pragma unroll 8
+    for (int kb = 0; kb < 32; ++kb) {
+      const double2 a = __ldcs(ap + kb * 32);
+      const double* b = s_r + (kb * 8 + q) * SR + g;
+      dmma(c0, a.x, b[0]);
+      dmma(c1, a.x, b[8]);
+      dmma(c0, a.y, b[4 * SR]);
+      dmma(c1, a.y, b[4 * SR + 8]);
+    }
+    const int col = mt * 8 + g;
+    if (col < d.m) {
+      double* dst = cpartm + (d.part_off + (long long)it.y * d.m + col) * MR;
+      *reinterpret_cast<double2*>(dst + 2 * q) = make_double2(c0[0], c0[1]);
+      *reinterpret_cast<double2*>(dst + 8 + 2 * q) = make_double2(c1[0], c1[1]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // chunk complete: the batched coarse solve may be waiting for it
+    __threadfence();
+    atomicAdd(blk_done + it.x, 1ull);
+  }
+}
+
+// U_b rows: a warp owns two 8-row tiles of a block and streams their packed fragments (at most
+// 2 x 8 loads, all issued before the first product); Y comes from [coarse column][16] through L1
+__global__ void __launch_bounds__(256) k_zy_multi_pk(const int2* __restrict__ items, int nitems,
+                                                     const CblkDesc* __restrict__ descs,
+                                                     const long long* __restrict__ zoff,
+                                                     const double2* __restrict__ zp, const double* __restrict__ ym,
+                                                     int nrhs, double* __restrict__ zsm, long long zs_len) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, g = lane >> 2;
+  const int iw = blockIdx.x * 8 + warp;
+  if (iw >= nitems) return;
+  const int2 it = items[iw];
+  const CblkDesc d = descs[it.x];
+  const int KB = (d.m + 7) >> 3, MT = (d.n + 7) >> 3;
+  const int mt0 = it.y * 2;
+  const bool two = mt0 + 1 < MT;
+  const double2* a0p = zp + (zoff[it.x] >> 1) + (size_t)mt0 * KB * 32 + lane;
+  const double2* a1p = two ? a0p + (size_t)KB * 32 : a0p;
+  const double* cp = ym + ((size_t)d.col0 + q) * MR + g;
+  double acc[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+  for (int kb0 = 0; kb0 < KB; kb0 += 8) {
+    double2 a0[8], a1[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int kb = min(kb0 + u, KB - 1);
+      a0[u] = __ldcs(a0p + kb * 32);
+      a1[u] = __ldcs(a1p + kb * 32);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int kb = kb0 + u;
+      if (kb < KB) {
+        const int k = kb * 8 + q;
+        const bool v0 = k < d.m, v1 = k + 4 < d.m;
+        const double* cu = cp + (size_t)kb * 8 * MR;
+        const double b00 = v0 ? __ldg(cu) : 0.0, b01 = v0 ? __ldg(cu + 8) : 0.0;
+        const double b10 = v1 ? __ldg(cu + 4 * MR) : 0.0, b11 = v1 ? __ldg(cu + 4 * MR + 8) : 0.0;
+        dmma(acc[0][0], a0[u].x, b00);
+        dmma(acc[0][1], a0[u].x, b01);
+        dmma(acc[1][0], a1[u].x, b00);
+        dmma(acc[1][1], a1[u].x, b01);
+        dmma(acc[0][0], a0[u].y, b10);
+        dmma(acc[0][1], a0[u].y, b11);
+        dmma(acc[1][0], a1[u].y, b10);
+        dmma(acc[1][1], a1[u].y, b11);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int row = (mt0 + t) * 8 + g;
+    if ((t == 1 && !two) || row >= d.n) continue;
+    double* dst = zsm + d.idx_off + row;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * h + 2 * q + e;
+        if (c < nrhs) dst[(long long)c * zs_len] = acc[t][h][e];
+      }
+  }
 }
 
 // ------------------------------------------------------------------ B0^{-1}
@@ -647,6 +817,37 @@ int multi_prepare(HgPrecond* P) {
       HG_CUDA_TRY(cudaMemset(P->d_cm, 0, sizeof(double) * MR * P->b0_mp));  // rows beyond m stay zero
       HG_TRY(alloc(&P->d_ypart, (size_t)B0_KSPLIT * MR * P->b0_mp));
     }
+    // packed copies of Z for the batched contractions (HG_Z_PACKED=0: the row-major kernels)
+    const char* zenv = getenv("HG_Z_PACKED");
+    if (!(zenv && zenv[0] == '0') && P->n_zt_items > 0) {
+      std::vector<long long> zoff(P->n_cblk), toff(P->n_cblk);
+      std::vector<int2> zit;
+      long long zlen = 0, tlen = 0;
+      for (int b = 0; b < P->n_cblk; ++b) {
+        const CblkDesc& d = P->h_cblk[b];
+        const long long KB = (d.m + 7) / 8, MT = (d.n + 7) / 8;
+        zoff[b] = zlen;
+        toff[b] = tlen;
+        zlen += MT * KB * 64;
+        tlen += (long long)d.nchunk * KB * 32 * 64;
+        if (d.m > 0)
+          for (int t = 0; t < (MT + 1) / 2; ++t) zit.push_back(make_int2(b, t));
+      }
+      HG_TRY(alloc(&P->d_zypk, (size_t)std::max(zlen, 1LL)));
+      HG_TRY(alloc(&P->d_ztpk, (size_t)std::max(tlen, 1LL)));
+      HG_CUDA_TRY(cudaMalloc(&P->d_zypk_off, sizeof(long long) * P->n_cblk));
+      HG_CUDA_TRY(cudaMalloc(&P->d_ztpk_off, sizeof(long long) * P->n_cblk));
+      HG_CUDA_TRY(cudaMemcpy(P->d_zypk_off, zoff.data(), sizeof(long long) * P->n_cblk, cudaMemcpyHostToDevice));
+      HG_CUDA_TRY(cudaMemcpy(P->d_ztpk_off, toff.data(), sizeof(long long) * P->n_cblk, cudaMemcpyHostToDevice));
+      HG_CUDA_TRY(cudaMalloc(&P->d_zy_items, sizeof(int2) * std::max<size_t>(zit.size(), 1)));
+      HG_CUDA_TRY(cudaMemcpy(P->d_zy_items, zit.data(), sizeof(int2) * zit.size(), cudaMemcpyHostToDevice));
+      P->n_zy_items = (int)zit.size();
+      k_zpack_zy<<<dim3(64, P->n_cblk), 256>>>(P->d_cblk, P->d_zypk_off, P->d_z, reinterpret_cast<double2*>(P->d_zypk));
+      HG_LAUNCH_CHECK();
+      k_zpack_zt<<<dim3(64, P->n_cblk), 256>>>(P->d_cblk, P->d_ztpk_off, P->d_z, reinterpret_cast<double2*>(P->d_ztpk));
+      HG_LAUNCH_CHECK();
+      HG_CUDA_TRY(cudaDeviceSynchronize());
+    }
     HG_CUDA_TRY(cudaMalloc(&P->d_blkm_done, sizeof(unsigned long long) * P->n_cblk));
     HG_CUDA_TRY(cudaMemset(P->d_blkm_done, 0, sizeof(unsigned long long) * P->n_cblk));
   }
@@ -660,6 +861,10 @@ int preload_multi() {
   HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_spmm));
   HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_zt_multi));
   HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_zy_multi));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_zt_multi_pk));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_zy_multi_pk));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_zpack_zy));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_zpack_zt));
   HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_b0_multi));
   HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_assemble_multi));
   HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_dots_batch));

@@ -272,3 +272,17 @@ def test_fov_bounds_batched_matches_reference_loop(cfg1):
     got = hg.fov_bounds(forms, small, mode="dense")
     want = _fov_reference_loop(forms, lambda u: orc.apply(forms.helmholtz @ u), "dense")
     assert abs(got[0] - want[0]) <= 1e-9 * abs(want[0]) and abs(got[1] - want[1]) <= 1e-9 * abs(want[1])
+
+
+def test_packed_z_matches_row_major_kernels(cfg1, monkeypatch):
+    """The batched Z^T R / Z Y read Z from packed DMMA-fragment copies (hg_multi.cu
+    "packed Z"); HG_Z_PACKED=0 keeps the row-major kernels.  Same products, same
+    k order: the two paths agree to rounding of the DMMA accumulation order."""
+    P, g, coarse, pre = cfg1
+    R = np.random.default_rng(21).standard_normal((pre.n, 16))
+    want = pre.apply_multi(R)
+    monkeypatch.setenv("HG_Z_PACKED", "0")
+    plain = hg.factorize(P.forms, P.dec, coarse)
+    got = plain.apply_multi(R)
+    assert colrel(got, want) <= 1e-13
+    assert colrel(plain.apply_multi(R[:, :3]), want[:, :3]) <= 1e-13
