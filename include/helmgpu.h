@@ -302,6 +302,14 @@ int hg_precond_spmv(HgPrecond* p, int which, const double* x, double* y, void* s
 /* Local solve of block s alone: x_local = B_s^{-1} r_local, both device,
  * length local_n[s] (LocalSolver.lu.solve). */
 int hg_local_solve(HgPrecond* p, int s, const double* r_local, double* x_local, void* stream);
+/* The one-level part before assembly: every block's local solution
+ * x_s = B_s^{-1} R_s r for a global residual r (device, n), written block
+ * after block to xs (device, local_idx_off[n_local] doubles; block s at
+ * local_idx_off[s]).  Includes the separator and spike stages of split
+ * blocks, whose solution is spread over their chunk blocks and their
+ * separator pseudo block — this is how LocalSolver.lu.solve of a split block
+ * is served (schwarz.py:26-34, 60). */
+int hg_precond_local_solutions(HgPrecond* p, const double* r, double* xs, void* stream);
 
 /* Stage timing of the apply (no reference analogue; measurement hook used by
  * bench.py): runs `iters` applies with the stages serialised on `stream`

@@ -107,6 +107,7 @@ SIGNATURES = {
     "hg_precond_spmv": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp]),
     "hg_precond_profile": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int32, _f64p, _vp]),
     "hg_local_solve": (ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp, _vp]),
+    "hg_precond_local_solutions": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "hg_op_create_csr": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, _i32p, _i32p, _f64p, ctypes.POINTER(_vp)]),
     "hg_op_create_precond": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_vp)]),
     "hg_op_destroy": (ctypes.c_int, [_vp]),

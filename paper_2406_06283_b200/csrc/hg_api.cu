@@ -1379,6 +1379,19 @@ int hg_local_solve(HgPrecond* P, int s, const double* r_local, double* x_local, 
   return launch_local_solve_single(P, s, r_local, x_local, (cudaStream_t)stream);
 }
 
+int hg_precond_local_solutions(HgPrecond* P, const double* r, double* xs, void* stream) {
+  if (!P || !r || !xs) {
+    set_error("hg_precond_local_solutions: null argument");
+    return HG_ERR_ARG;
+  }
+  HG_TRY(precond_fault(P));
+  if (P->n_local == 0 || P->xs_len == 0) return HG_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  HG_TRY(launch_local_solve(P, r, st));
+  HG_CUDA_TRY(cudaMemcpyAsync(xs, P->d_xs, sizeof(double) * (size_t)P->xs_len, cudaMemcpyDeviceToDevice, st));
+  return HG_OK;
+}
+
 int hg_op_create_csr(int32_t n, int64_t nnz, const int32_t* indptr, const int32_t* indices, const double* data,
                      HgOp** out) {
   if (!out || n <= 0 || !indptr || (nnz > 0 && (!indices || !data))) {

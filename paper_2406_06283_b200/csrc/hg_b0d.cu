@@ -142,7 +142,7 @@ __global__ void k_creduce_multi(int m, int nrhs, const int* __restrict__ col_blk
 // tiles (4 DMMA accumulators for the 16 columns), streams their packed fragments and takes the B
 // fragments of C (fragment order, zero padded; 2 MB, L1 / L2 resident) straight from global memory —
 // no shared memory, no barrier.
-__global__ void __launch_bounds__(256) k_b0_gemm_multi(int mp, const double2* __restrict__ Bpk,
+__global__ void __launch_bounds__(256, 3) k_b0_gemm_multi(int mp, const double2* __restrict__ Bpk,
                                                        const double* __restrict__ C, double* __restrict__ Yp) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, g = lane >> 2;
   const int KB = mp >> 3;

@@ -188,16 +188,31 @@ def _split_all(todo):
 
 class SplitLocalLU:
     """``LocalSolver.lu`` of a subdomain whose block is split into chunks and
-    separators (factor.split_block): its solve exists only inside the
-    preconditioner apply (chunk solves, separator system and spike update are
-    three device stages over all subdomains at once)."""
+    separators (factor.split_block).  Its solve is three device stages over
+    ALL subdomains (chunk solves, separator systems, spike updates), so
+    ``solve`` runs the whole one-level part on a residual supported on this
+    subdomain's dofs (hg_precond_local_solutions) and reads this subdomain's
+    pieces back: the same B_s^{-1} r as an unsplit block's hg_local_solve."""
 
-    def __init__(self, n):
-        self.shape = (n, n)
+    def __init__(self, precond, idof, pieces):
+        self._p = precond
+        self._idof = np.asarray(idof)
+        self._pieces = pieces  # [(block-local rows, position in the local solution scratch)]
+        self.shape = (self._idof.size, self._idof.size)
 
     def solve(self, rhs):
-        raise NotImplementedError("this subdomain's block is split (HG_LOCAL_SPLIT); its local solve runs inside "
-                                  "apply() / apply_multi()")
+        torch = _torch()
+        p = self._p
+        t, was_np = _as_device(rhs, self._idof.size)
+        r = torch.zeros(p.n, dtype=torch.float64, device=t.device)
+        r[torch.from_numpy(self._idof).to(t.device)] = t
+        xs = torch.empty(p.xs_len, dtype=torch.float64, device=t.device)
+        _lib.check(_lib.load().hg_precond_local_solutions(p._handle, _vp(r), _vp(xs), _stream()),
+                   "hg_precond_local_solutions")
+        out = torch.empty_like(t)
+        for rows, pos in self._pieces:
+            out[torch.from_numpy(rows).to(t.device)] = xs[pos:pos + rows.size]
+        return out.cpu().numpy() if was_np else out
 
 
 class LocalSolver:
@@ -378,7 +393,13 @@ class TwoLevelPreconditioner:
         self._upload(B, Dk, factors, cblocks, lu, piv)
         for s, ls in enumerate(self.local_solvers):
             b = self._dev_block[s]
-            ls.lu = GpuBandLU(self, b, factors[b][1], s) if b is not None else SplitLocalLU(ls.idof.size)
+            ls.lu = GpuBandLU(self, b, factors[b][1], s) if b is not None else None
+        off = np.concatenate([[0], np.cumsum([i.size for i, _ in factors])])
+        self.xs_len = int(off[-1])
+        for s, sb, b0 in self.splits:
+            pieces = [(rows, int(off[b0 + p])) for p, (rows, _) in enumerate(sb.chunks)]
+            pieces.append((sb.sep_rows, int(off[b0 + len(sb.chunks)])))
+            self.local_solvers[s].lu = SplitLocalLU(self, self.local_solvers[s].idof, pieces)
 
     @staticmethod
     def _split_chunks(blocks, bws):
@@ -474,8 +495,10 @@ class TwoLevelPreconditioner:
             idof = np.asarray(idx[off[s]:off[s + 1]], dtype=np.int64)
             kl, kv = meta["local_bands"][s]
             ls = LocalSolver(ci, fi, idof, None, np.nan, None, matrix=self._B)
-            if idof.size and int(arrays["local_n"][s]) == 0:  # separator pseudo block of a split subdomain
-                ls.lu = SplitLocalLU(int(idof.size))
+            if idof.size and int(arrays["local_n"][s]) == 0:
+                # separator pseudo block of a split subdomain (a cached image lists device blocks,
+                # not subdomains): no solve of its own
+                ls.lu = None
             else:
                 ls.lu = GpuBandLU(self, s, types.SimpleNamespace(n=int(idof.size), kl=kl, kv=kv))
             self.local_solvers.append(ls)
@@ -785,6 +808,7 @@ class TwoLevelPreconditioner:
         self._meta = meta
         self.m = int(meta["m"])
         self.local_sizes = [int(x) for x in arrays["local_n"]] if "local_n" in arrays else []
+        self.xs_len = int(np.asarray(arrays["local_idx_off"])[-1]) if "local_idx_off" in arrays else 0
         self.local_bands = [tuple(b) for b in meta["local_bands"]]
         self.cblock_shapes = [tuple(c) for c in meta["cblock_shapes"]]
         self.b0_bytes = int(meta["b0_bytes"])

@@ -54,8 +54,10 @@ def test_split_apply_matches_unsplit_and_oracle(cfg3, nchunk, monkeypatch):
     assert np.array_equal(pre.apply(r), got)
     s = rng.standard_normal(pre.n)
     assert rel(pre.apply(2.0 * r - 3.0 * s), 2.0 * got - 3.0 * pre.apply(s)) <= 1e-12
-    with pytest.raises(NotImplementedError):
-        pre.local_solvers[0].lu.solve(np.zeros(pre.local_solvers[0].idof.size))
+    # LocalSolver.lu.solve of a split block (schwarz.py:26-34) against the unsplit block's device solve
+    for s in (0, len(pre.local_solvers) - 1):
+        rl = rng.standard_normal(pre.local_solvers[s].idof.size)
+        assert rel(pre.local_solvers[s].lu.solve(rl), plain.local_solvers[s].lu.solve(rl)) <= 1e-11
 
 
 def test_split_gmres_matches_oracle(cfg3, monkeypatch):

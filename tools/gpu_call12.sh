@@ -1,0 +1,4 @@
+export HG_CACHE_DIR=/tmp/hgcache_r2
+set -x
+python tools/prof_stages.py 5-16 2>&1 | grep -v Warn
+python -m pytest tests/test_gpu_multi.py -m gpu -x -q 2>&1 | tail -2
