@@ -530,7 +530,8 @@ def run_ours(args, dist):
         "setup_s": {k: round(v, 2) for k, v in setup.items()},
         "setup_device": {"local_factor": bool(getattr(pre, "device_factor", False)),
                          "coarse_operator": bool(cb and cb.get("device")),
-                         "gevp": getattr(args, "gevp", "auto")},
+                         "gevp": getattr(args, "gevp", "auto"),
+                         "local_split_subdomains": int(getattr(pre, "n_split", 0))},
         "gpu_launches": launches,
         "clocks": clk,
     }

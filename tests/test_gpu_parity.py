@@ -288,3 +288,29 @@ def test_weighted_basis_orthonormality(orth):
     for c in range(2):
         Vc = op.basis(40, col=c).cpu().numpy().T
         assert np.abs(Vc.T @ (W @ Vc) - np.eye(40)).max() <= 1e-10
+
+
+def test_local_solutions_match_block_solves(cfg1):
+    """hg_precond_local_solutions: every block's x_s = B_s^{-1} R_s r before assembly equals the
+    block-by-block LocalSolver.lu.solve (schwarz.py:58-60), and summing them is the one-level apply."""
+    import ctypes
+
+    import torch
+
+    from paper_2406_06283_b200 import _lib
+
+    P, g, coarse, pre = cfg1
+    r = np.random.default_rng(8).standard_normal(pre.n)
+    rd = torch.from_numpy(r).cuda()
+    xs = torch.empty(pre.xs_len, dtype=torch.float64, device="cuda")
+    _lib.check(_lib.load().hg_precond_local_solutions(pre._handle, ctypes.c_void_p(rd.data_ptr()),
+                                                      ctypes.c_void_p(xs.data_ptr()), None), "local_solutions")
+    xs = xs.cpu().numpy()
+    pos = 0
+    acc = np.zeros(pre.n)
+    for ls in pre.local_solvers:
+        n = ls.idof.size
+        assert np.array_equal(xs[pos:pos + n], ls.lu.solve(r[ls.idof]))
+        np.add.at(acc, ls.idof, xs[pos:pos + n])
+        pos += n
+    assert pos == pre.xs_len
