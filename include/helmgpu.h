@@ -61,7 +61,7 @@ extern "C" {
 #define HG_ERR_UNSUPPORTED 3
 #define HG_ERR_NOMEM 4
 
-#define HG_ABI_VERSION 4
+#define HG_ABI_VERSION 5
 
 /* Most right-hand sides one batched call handles (BASELINE config 5's
  * batch of 16 seeded load vectors). */
@@ -223,6 +223,40 @@ typedef struct {
   const int64_t* spike_off;       /* n_spike, in doubles */
   int64_t spike_len;
   const double* spike_data;
+
+  /* Bisected coarse solve (optional; b0_split = 0: none).  The single-RHS
+   * coarse solve y = B0^{-1} c (lu_solve, schwarz.py:56) is a chain of 2K
+   * panel hand-offs; B0 is banded (subdomains couple to their neighbours
+   * only), so — like a split local block — its unknowns are cut into two
+   * halves H0 = [0, a), H1 = [a + ns, m) and a separator S = [a, a + ns)
+   * (ns >= B0's bandwidth): the halves' chains (their own getrf tiles, in
+   * the layout of b0_* above; cluster mode only) run side by side on two
+   * clusters, then x_S = Sigma^{-1} (c_S - F y_H), y_H -= W x_S with
+   * Sigma = B0_SS - sum_h B0_SHh B0_HhHh^{-1} B0_HhS, F = [B0[S, a-wl..a),
+   * B0[S, a+ns..a+ns+wr)] (ns x (wl + wr), row-major: everything B0_SH is
+   * nonzero on) and W = [B0_H0H0^{-1} B0_H0S; B0_H1H1^{-1} B0_H1S]
+   * ((m - ns) x ns, row-major).  Same operator, different elimination
+   * order; the caller checks it against getrs (bar 1e-11).  Batched applies
+   * are not affected (they use b0_inv). */
+  int32_t b0_split;
+  int32_t b0s_a, b0s_ns, b0s_wl, b0s_wr;
+  int32_t b0h0_npanel, b0h0_ring, b0h0_cluster;
+  int64_t b0h0_ntile;
+  const int32_t* b0h0_perm;      /* a */
+  const double* b0h0_dinv;
+  const int64_t* b0h0_tile_ptr;
+  const int32_t* b0h0_tile_col;
+  const double* b0h0_tiles;
+  int32_t b0h1_npanel, b0h1_ring, b0h1_cluster;
+  int64_t b0h1_ntile;
+  const int32_t* b0h1_perm;      /* m - a - ns */
+  const double* b0h1_dinv;
+  const int64_t* b0h1_tile_ptr;
+  const int32_t* b0h1_tile_col;
+  const double* b0h1_tiles;
+  const double* b0s_f;
+  const double* b0s_sinv;
+  const double* b0s_w;
 } HgPrecondDesc;
 
 /* ---- library ---- */
@@ -405,6 +439,11 @@ int64_t hg_dcgs2_explicit_passes(void);
 #define HG_DEBUG_SPIN_LIMIT_MS 1
 #define HG_DEBUG_SKIP_ZT 2
 #define HG_DEBUG_FORCE_EXPLICIT_RHO 3
+/* 0: the single-RHS coarse solve runs the full panel chain even when the handle has the bisected one */
+#define HG_DEBUG_B0_SPLIT 4
+/* ring stages of the single-RHS local solve (4..6; fewer stages = less shared memory = more CTAs
+ * per SM beside the coarse chains) */
+#define HG_DEBUG_LOCAL_STAGES 5
 int hg_debug_set(HgPrecond* p, int32_t key, int64_t value);
 
 /* Krylov basis of the last hg_gmres / hg_gmres_batch solve on `op`

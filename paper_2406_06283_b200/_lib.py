@@ -88,6 +88,32 @@ class HgPrecondDesc(ctypes.Structure):
         ("spike_off", _i64p),
         ("spike_len", ctypes.c_int64),
         ("spike_data", _f64p),
+        ("b0_split", ctypes.c_int32),
+        ("b0s_a", ctypes.c_int32),
+        ("b0s_ns", ctypes.c_int32),
+        ("b0s_wl", ctypes.c_int32),
+        ("b0s_wr", ctypes.c_int32),
+        ("b0h0_npanel", ctypes.c_int32),
+        ("b0h0_ring", ctypes.c_int32),
+        ("b0h0_cluster", ctypes.c_int32),
+        ("b0h0_ntile", ctypes.c_int64),
+        ("b0h0_perm", _i32p),
+        ("b0h0_dinv", _f64p),
+        ("b0h0_tile_ptr", _i64p),
+        ("b0h0_tile_col", _i32p),
+        ("b0h0_tiles", _f64p),
+        ("b0h1_npanel", ctypes.c_int32),
+        ("b0h1_ring", ctypes.c_int32),
+        ("b0h1_cluster", ctypes.c_int32),
+        ("b0h1_ntile", ctypes.c_int64),
+        ("b0h1_perm", _i32p),
+        ("b0h1_dinv", _f64p),
+        ("b0h1_tile_ptr", _i64p),
+        ("b0h1_tile_col", _i32p),
+        ("b0h1_tiles", _f64p),
+        ("b0s_f", _f64p),
+        ("b0s_sinv", _f64p),
+        ("b0s_w", _f64p),
     ]
 
 
@@ -155,8 +181,8 @@ SIGNATURES = {
 STAT_PANEL_ACTIVE, STAT_PANEL_DEVIATION, STAT_PANEL_BYTES = 1, 2, 3
 FIELD_LOCAL_FWD, FIELD_LOCAL_BWD = 1, 2
 
-ABI_VERSION = 4
-DEBUG_SPIN_LIMIT_MS, DEBUG_SKIP_ZT, DEBUG_FORCE_EXPLICIT_RHO = 1, 2, 3
+ABI_VERSION = 5
+DEBUG_SPIN_LIMIT_MS, DEBUG_SKIP_ZT, DEBUG_FORCE_EXPLICIT_RHO, DEBUG_B0_SPLIT, DEBUG_LOCAL_STAGES = 1, 2, 3, 4, 5
 MAX_BASIS = 1024  # Krylov vectors the basis kernels support (MAX_NV)
 NPHASES = 7  # HG_NPHASES
 ORTH = {"measured": 0, "dcgs2": 1}

@@ -33,8 +33,8 @@ import numpy as np
 import scipy.sparse as sp
 
 CACHE_VERSION = 1
-SETUP_VERSION = "r2b"  # bump when the host setup restatement changes its outputs
-KNOBS = ("HG_B0_MODE", "HG_B0_PANEL", "HG_B0_DENSE", "HG_B0_CTAS", "HG_LOCAL_SPLIT")
+SETUP_VERSION = "r2c"  # bump when the host setup restatement changes its outputs
+KNOBS = ("HG_B0_MODE", "HG_B0_PANEL", "HG_B0_DENSE", "HG_B0_CTAS", "HG_LOCAL_SPLIT", "HG_B0_SPLIT", "HG_B0_SPLIT_CS")
 
 
 def default_dir():

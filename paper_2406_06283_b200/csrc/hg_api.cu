@@ -535,11 +535,21 @@ static int precond_apply_core_impl(HgPrecond* P, const double* r, double* out, c
     HG_CUDA_TRY(cudaEventRecord(P->ev_fork, st));
     HG_CUDA_TRY(cudaStreamWaitEvent(P->aux, P->ev_fork, 0));
     const bool ser = serial_order(st);
+    bool zt_launched = false;
     if (ser) {
       // tools that serialise kernels (profilers, sanitizers, blocking launches)
       // and graph capture: no kernel may wait on a later one
       HG_TRY(launch_zt(P, r, P->aux));
       HG_TRY(launch_coarse_solve(P, P->aux));
+    } else if (P->b0_split_on && P->b0_mode == 1) {
+      // bisected coarse solve: the two half chains first (they hold their SMs and wait, bounded,
+      // for their rows' Z^T r chunks); the separator stage reads c_S, i.e. needs ALL of Z^T r
+      HG_TRY(launch_coarse_chains_split(P, P->aux));
+      HG_TRY(launch_zt(P, r, st));
+      HG_CUDA_TRY(cudaEventRecord(P->ev_zt, st));
+      HG_CUDA_TRY(cudaStreamWaitEvent(P->aux, P->ev_zt, 0));
+      HG_TRY(launch_coarse_sep_split(P, P->aux));
+      zt_launched = true;
     } else {
       // The latency-bound coarse solve is launched FIRST (side stream) so that
       // it holds its SMs before the local solves fill the GPU; it starts its
@@ -549,7 +559,7 @@ static int precond_apply_core_impl(HgPrecond* P, const double* r, double* out, c
     }
     HG_TRY(launch_zy(P, P->aux));
     HG_CUDA_TRY(cudaEventRecord(P->ev_join, P->aux));
-    if (!ser) HG_TRY(launch_zt(P, r, st));
+    if (!ser && !zt_launched) HG_TRY(launch_zt(P, r, st));
   }
   HG_TRY(launch_local_solve(P, r, st));
   if (P->m > 0) HG_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_join, 0));
@@ -807,6 +817,21 @@ int hg_precond_destroy(HgPrecond* P) {
   P->d_fault = nullptr;
   release(P->d_tmpm);
   if (P->aux) cudaStreamDestroy(P->aux);
+  if (P->aux2) cudaStreamDestroy(P->aux2);
+  for (cudaEvent_t e : {P->ev_c0, P->ev_c1, P->ev_zt})
+    if (e) cudaEventDestroy(e);
+  for (auto& c : P->b0h) {
+    release(c.perm);
+    release(c.dinv);
+    release(c.tile_ptr);
+    release(c.tile_col);
+    release(c.tiles);
+    release(c.xbuf);
+  }
+  release(P->d_b0s_f);
+  release(P->d_b0s_sinv);
+  release(P->d_b0s_w);
+  release(P->d_b0s_t);
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);
   if (P->ev_join) cudaEventDestroy(P->ev_join);
   hg_op_destroy(P->op_T);
@@ -1059,6 +1084,66 @@ static int precond_create_impl(const HgPrecondDesc* D, HgPrecond* P) {
     HG_TRY(upload<unsigned long long>(&P->d_blk_done, nullptr, (size_t)D->n_cblk, bytes));
     HG_CUDA_TRY(cudaMemset(P->d_blk_done, 0, sizeof(unsigned long long) * D->n_cblk));
     HG_TRY(upload<double>(&P->d_y, nullptr, (size_t)P->m, bytes));
+    if (D->b0_split) {  // bisected single-RHS coarse solve
+      const int a = D->b0s_a, ns = D->b0s_ns;
+      if (P->b0_mode != 1 || a <= 0 || ns <= 0 || a + ns >= P->m || D->b0s_wl < 0 || D->b0s_wl > a ||
+          D->b0s_wr < 0 || a + ns + D->b0s_wr > P->m || !D->b0s_f || !D->b0s_sinv || !D->b0s_w || !D->b0h0_perm ||
+          !D->b0h1_perm || !D->b0h0_dinv || !D->b0h1_dinv || !D->b0h0_tile_ptr || !D->b0h1_tile_ptr) {
+        set_error("hg_precond_create: inconsistent bisected coarse solve (needs the cluster mode)");
+        return HG_ERR_ARG;
+      }
+      const int hm[2] = {a, P->m - a - ns}, hoff[2] = {0, a + ns};
+      const int hk[2] = {D->b0h0_npanel, D->b0h1_npanel}, hr[2] = {D->b0h0_ring, D->b0h1_ring};
+      const int hc[2] = {D->b0h0_cluster, D->b0h1_cluster};
+      const long long hnt[2] = {D->b0h0_ntile, D->b0h1_ntile};
+      const int32_t* hperm[2] = {D->b0h0_perm, D->b0h1_perm};
+      const double* hdinv[2] = {D->b0h0_dinv, D->b0h1_dinv};
+      const int64_t* hptr[2] = {D->b0h0_tile_ptr, D->b0h1_tile_ptr};
+      const int32_t* hcol[2] = {D->b0h0_tile_col, D->b0h1_tile_col};
+      const double* htiles[2] = {D->b0h0_tiles, D->b0h1_tiles};
+      for (int h = 0; h < 2; ++h) {
+        HgPrecond::B0Half& c = P->b0h[h];
+        c.m = hm[h];
+        c.off = hoff[h];
+        c.K = hk[h];
+        c.nr = hr[h];
+        c.cs = hc[h];
+        if (c.K != (c.m + 63) / 64 || c.cs < 1 || c.cs > 16 || c.nr < c.cs + 1 ||
+            b0_cluster_smem(c.nr) > 227 * 1024 || (hnt[h] > 0 && (!hcol[h] || !htiles[h]))) {
+          set_error("hg_precond_create: invalid half-chain parameters of the bisected coarse solve");
+          return HG_ERR_ARG;
+        }
+        std::vector<int> gperm(c.m);  // chain row -> global coarse column
+        for (int i = 0; i < c.m; ++i) {
+          if (hperm[h][i] < 0 || hperm[h][i] >= c.m) {
+            set_error("hg_precond_create: half-chain permutation out of range");
+            return HG_ERR_ARG;
+          }
+          gperm[i] = c.off + hperm[h][i];
+        }
+        HG_TRY(upload(&c.perm, gperm.data(), gperm.size(), bytes));
+        HG_TRY(upload(&c.dinv, hdinv[h], (size_t)2 * c.K * 64 * 64, bytes));
+        HG_TRY(upload(&c.tile_ptr, reinterpret_cast<const long long*>(hptr[h]), (size_t)2 * c.K + 1, bytes));
+        if (hnt[h] > 0) {
+          HG_TRY(upload(&c.tile_col, hcol[h], (size_t)hnt[h], bytes));
+          HG_TRY(upload(&c.tiles, htiles[h], (size_t)hnt[h] * 64 * 64, bytes));
+        }
+        HG_TRY(upload<double>(&c.xbuf, nullptr, (size_t)2 * c.K * 64, bytes));
+      }
+      P->b0s_a = a;
+      P->b0s_ns = ns;
+      P->b0s_wl = D->b0s_wl;
+      P->b0s_wr = D->b0s_wr;
+      HG_TRY(upload(&P->d_b0s_f, D->b0s_f, (size_t)ns * (D->b0s_wl + D->b0s_wr), bytes));
+      HG_TRY(upload(&P->d_b0s_sinv, D->b0s_sinv, (size_t)ns * ns, bytes));
+      HG_TRY(upload(&P->d_b0s_w, D->b0s_w, (size_t)(P->m - ns) * ns, bytes));
+      HG_TRY(upload<double>(&P->d_b0s_t, nullptr, (size_t)ns, bytes));
+      HG_CUDA_TRY(cudaStreamCreateWithFlags(&P->aux2, cudaStreamNonBlocking));
+      HG_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_c0, cudaEventDisableTiming));
+      HG_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_c1, cudaEventDisableTiming));
+      HG_CUDA_TRY(cudaEventCreateWithFlags(&P->ev_zt, cudaEventDisableTiming));
+      P->b0_split = P->b0_split_on = true;
+    }
     if (D->b0_inv) {
       // row-major in (host or device memory), kept packed in DMMA-fragment order
       double* rowmajor = nullptr;
@@ -1293,6 +1378,36 @@ int hg_debug_set(HgPrecond* P, int32_t key, int64_t value) {
     case HG_DEBUG_FORCE_EXPLICIT_RHO:
       g_force_explicit_rho = value != 0;
       return HG_OK;
+    case HG_DEBUG_LOCAL_STAGES:
+      if (!P) break;
+      if (value != 0 && (value < 2 || value > 6)) {
+        set_error("hg_debug_set: local stages must be 0 (default) or 2..6");
+        return HG_ERR_ARG;
+      }
+      P->ls_ns = (int)value;
+      return HG_OK;
+    case HG_DEBUG_B0_SPLIT: {
+      if (!P) break;
+      if (!P->b0_split) return HG_OK;  // nothing to switch
+      // the chains pair with Z^T r launches through device tickets: bring the tickets of the
+      // chains that sat out up to the number of Z^T r launches so far
+      HG_CUDA_TRY(cudaDeviceSynchronize());
+      unsigned long long done = 0;
+      int b0 = -1;
+      for (int b = 0; b < P->n_cblk && b0 < 0; ++b)
+        if (P->h_cblk[b].nchunk > 0) b0 = b;
+      if (b0 >= 0) {
+        HG_CUDA_TRY(cudaMemcpy(&done, P->d_blk_done + b0, sizeof(done), cudaMemcpyDeviceToHost));
+        const unsigned long long launches = done / (unsigned long long)P->h_cblk[b0].nchunk;
+        const unsigned long long t[3] = {launches * (unsigned long long)P->b0_cs,
+                                         launches * (unsigned long long)P->b0h[0].cs,
+                                         launches * (unsigned long long)P->b0h[1].cs};
+        HG_CUDA_TRY(cudaMemcpy(P->d_ticket, &t[0], sizeof(unsigned long long), cudaMemcpyHostToDevice));
+        HG_CUDA_TRY(cudaMemcpy(P->d_ticket + 2, &t[1], 2 * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+      }
+      P->b0_split_on = value != 0;
+      return HG_OK;
+    }
     default:
       break;
   }

@@ -314,34 +314,120 @@ size_t b0_cluster_smem(int NR) {
          sizeof(uint64_t) * (2 * TNS + 1);
 }
 
-int preload_b0_cluster() {
-  cudaFuncAttributes at;
-  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_b0_cluster));
-  return HG_OK;
-}
-
-int launch_coarse_solve_cluster(HgPrecond* P, cudaStream_t st) {
-  const int K = P->b0_K;
-  const int CS = P->b0_cs;
-  B0ClusterArgs a{P->m, K, P->b0_nr, CS, P->d_b0_perm, P->d_col_blk, P->d_cblk, P->d_cpart, P->d_b0_dinv,
-                  P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles, P->d_b0_x, P->d_y,
-                  P->d_blk_done, P->d_ticket, spin_cfg(P)};
-  const size_t smem = b0_cluster_smem(P->b0_nr);
+static int launch_chain(const B0ClusterArgs& a, cudaStream_t st) {
+  const size_t smem = b0_cluster_smem(a.NR);
   HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k_b0_cluster), smem, true));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(CS);
+  cfg.gridDim = dim3(a.CS);
   cfg.blockDim = dim3(CTHREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.x = a.CS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   HG_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_b0_cluster, a));
   HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+// ---- bisected coarse solve (helmgpu.h "Bisected coarse solve"): separator stage, one warp per row
+namespace {
+__device__ __forceinline__ double warp_dot(const double* __restrict__ a, const double* __restrict__ x, int n, int lane) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int k = lane;
+  for (; k + 96 < n; k += 128) {
+    s0 = fma(__ldcs(a + k), __ldg(x + k), s0);
+    s1 = fma(__ldcs(a + k + 32), __ldg(x + k + 32), s1);
+    s2 = fma(__ldcs(a + k + 64), __ldg(x + k + 64), s2);
+    s3 = fma(__ldcs(a + k + 96), __ldg(x + k + 96), s3);
+  }
+  for (; k < n; k += 32) s0 = fma(__ldcs(a + k), __ldg(x + k), s0);
+  return warp_sum((s0 + s1) + (s2 + s3));
+}
+}  // namespace
+
+// t = c_S - F [y[a - wl, a); y[a + ns, a + ns + wr)]; c_S from the Z^T r partials (fixed chunk order)
+__global__ void __launch_bounds__(256) k_b0s_t(int ns, int wl, int wr, int a, const double* __restrict__ F,
+                                               const double* __restrict__ y, const int* __restrict__ col_blk,
+                                               const CblkDesc* __restrict__ descs, const double* __restrict__ cpart,
+                                               double* __restrict__ t) {
+  const int k = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (k >= ns) return;
+  const double* f = F + (size_t)k * (wl + wr);
+  const double s = warp_dot(f, y + a - wl, wl, lane) + warp_dot(f + wl, y + a + ns, wr, lane);
+  if (lane == 0) {
+    const CblkDesc d = descs[col_blk[a + k]];
+    const int l = a + k - d.col0;
+    double c = 0.0;
+    for (int ch = 0; ch < d.nchunk; ++ch) c += cpart[d.part_off + (long long)ch * d.m + l];
+    t[k] = c - s;
+  }
+}
+
+// x_S = Sigma^{-1} t, written to y[a ..)
+__global__ void __launch_bounds__(256) k_b0s_x(int ns, const double* __restrict__ Sinv, const double* __restrict__ t,
+                                               double* __restrict__ ys) {
+  const int k = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (k >= ns) return;
+  const double s = warp_dot(Sinv + (size_t)k * ns, t, ns, lane);
+  if (lane == 0) ys[k] = s;
+}
+
+// y_H -= W x_S (row r of W belongs to coarse unknown r for r < a, r + ns beyond)
+__global__ void __launch_bounds__(256) k_b0s_w(int m, int ns, int a, const double* __restrict__ W, double* __restrict__ y) {
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= m - ns) return;
+  const double s = warp_dot(W + (size_t)r * ns, y + a, ns, lane);
+  const int i = r < a ? r : r + ns;
+  if (lane == 0) y[i] -= s;
+}
+
+static B0ClusterArgs half_args(HgPrecond* P, int h) {
+  const HgPrecond::B0Half& c = P->b0h[h];
+  return B0ClusterArgs{c.m, c.K, c.nr, c.cs, c.perm, P->d_col_blk, P->d_cblk, P->d_cpart, c.dinv,
+                       c.tile_ptr, c.tile_col, c.tiles, c.xbuf, P->d_y + c.off,
+                       P->d_blk_done, P->d_ticket + 2 + h, spin_cfg(P)};
+}
+
+// both half chains side by side (half 1 on the handle's second side stream), joined on st
+int launch_coarse_chains_split(HgPrecond* P, cudaStream_t st) {
+  HG_CUDA_TRY(cudaEventRecord(P->ev_c0, st));
+  HG_CUDA_TRY(cudaStreamWaitEvent(P->aux2, P->ev_c0, 0));
+  HG_TRY(launch_chain(half_args(P, 1), P->aux2));
+  HG_CUDA_TRY(cudaEventRecord(P->ev_c1, P->aux2));
+  HG_TRY(launch_chain(half_args(P, 0), st));
+  HG_CUDA_TRY(cudaStreamWaitEvent(st, P->ev_c1, 0));
+  return HG_OK;
+}
+
+// separator stage; the caller has ordered st after the whole Z^T r (c_S is read here)
+int launch_coarse_sep_split(HgPrecond* P, cudaStream_t st) {
+  const int ns = P->b0s_ns, a = P->b0s_a;
+  k_b0s_t<<<ceil_div(ns, 8), 256, 0, st>>>(ns, P->b0s_wl, P->b0s_wr, a, P->d_b0s_f, P->d_y, P->d_col_blk, P->d_cblk,
+                                           P->d_cpart, P->d_b0s_t);
+  HG_LAUNCH_CHECK();
+  k_b0s_x<<<ceil_div(ns, 8), 256, 0, st>>>(ns, P->d_b0s_sinv, P->d_b0s_t, P->d_y + a);
+  HG_LAUNCH_CHECK();
+  k_b0s_w<<<ceil_div(P->m - ns, 8), 256, 0, st>>>(P->m, ns, a, P->d_b0s_w, P->d_y);
+  HG_LAUNCH_CHECK();
+  return HG_OK;
+}
+
+int launch_coarse_solve_cluster(HgPrecond* P, cudaStream_t st) {
+  if (P->b0_split_on) {  // serial contexts: Z^T r (or its stand-in) precedes on this stream
+    HG_TRY(launch_coarse_chains_split(P, st));
+    return launch_coarse_sep_split(P, st);
+  }
+  const int K = P->b0_K;
+  const int CS = P->b0_cs;
+  B0ClusterArgs a{P->m, K, P->b0_nr, CS, P->d_b0_perm, P->d_col_blk, P->d_cblk, P->d_cpart, P->d_b0_dinv,
+                  P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles, P->d_b0_x, P->d_y,
+                  P->d_blk_done, P->d_ticket, spin_cfg(P)};
+  HG_TRY(launch_chain(a, st));
   static const bool stamps = getenv("HG_B0_STAMPS") != nullptr;
   if (stamps) {  // timing experiment: SM-cycle breakdown of the panel hand-off
     static bool armed = false;
@@ -372,6 +458,15 @@ int launch_coarse_solve_cluster(HgPrecond* P, cudaStream_t st) {
     for (int g = 0; g < n; ++g) h[4 * g + 1] = 0;
     HG_CUDA_TRY(cudaMemcpyToSymbol(g_b0c_stamps, h.data(), sizeof(unsigned long long) * h.size()));
   }
+  return HG_OK;
+}
+
+int preload_b0_cluster() {
+  cudaFuncAttributes at;
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_b0_cluster));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_b0s_t));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_b0s_x));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_b0s_w));
   return HG_OK;
 }
 

@@ -53,6 +53,7 @@ struct HgPrecond {
   // one-level part
   int n_local = 0;
   int rf = 0, rb = 0;            // register tiles (rows/32) of the two sweeps
+  int ls_ns = 0;                 // ring stages of the row solve (0 = the default 6; hg_debug_set)
   int max_fstride = 0, max_bstride = 0;
   hg::LocalDesc* d_local = nullptr;
   std::vector<hg::LocalDesc> h_local;
@@ -88,6 +89,27 @@ struct HgPrecond {
   int2* d_spike_items1 = nullptr;   // (spike, 8-row tile)
   int2* d_spike_items2 = nullptr;   // (spike, pair of 8-row tiles)
   double* d_xsep = nullptr;         // [separator row][HG_MAX_RHS] compact x_S
+
+  // bisected single-RHS coarse solve (hg_b0c.cu, helmgpu.h "Bisected coarse solve")
+  struct B0Half {
+    int m = 0, K = 0, nr = 0, cs = 0, off = 0;
+    int* perm = nullptr;            // chain row -> global coarse column
+    double* dinv = nullptr;
+    long long* tile_ptr = nullptr;
+    int* tile_col = nullptr;
+    double* tiles = nullptr;
+    double* xbuf = nullptr;
+  };
+  bool b0_split = false;            // bisected data present
+  bool b0_split_on = false;         // ... and in use (hg_debug_set can switch it off)
+  B0Half b0h[2];
+  int b0s_a = 0, b0s_ns = 0, b0s_wl = 0, b0s_wr = 0;
+  double* d_b0s_f = nullptr;
+  double* d_b0s_sinv = nullptr;
+  double* d_b0s_w = nullptr;
+  double* d_b0s_t = nullptr;
+  cudaStream_t aux2 = nullptr;
+  cudaEvent_t ev_c0 = nullptr, ev_c1 = nullptr, ev_zt = nullptr;
 
   // coarse part
   int m = 0;
@@ -228,6 +250,9 @@ int launch_zt(HgPrecond* P, const double* r, cudaStream_t st);
 // the solve waits (bounded, device side) for the Z^T r launch it pairs with
 int launch_coarse_solve(HgPrecond* P, cudaStream_t st);
 int launch_coarse_solve_cluster(HgPrecond* P, cudaStream_t st);
+// bisected coarse solve: the two half chains (joined on st), then the separator stage
+int launch_coarse_chains_split(HgPrecond* P, cudaStream_t st);
+int launch_coarse_sep_split(HgPrecond* P, cudaStream_t st);
 SpinCfg spin_cfg(const HgPrecond* P);
 // per (kernel, device) dynamic shared memory / cluster attributes (thread safe)
 int ensure_func_attrs(const void* func, size_t smem, bool nonportable_cluster);

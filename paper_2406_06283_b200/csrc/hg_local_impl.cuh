@@ -40,7 +40,7 @@
 namespace hg {
 
 constexpr int LS_CH = 16;  // steps per staged chunk
-constexpr int LS_NS = 6;   // ring stages
+constexpr int LS_NS = 6;   // ring stages at most (runtime count: HgPrecond::ls_ns, 4 or 6)
 constexpr int LS_THREADS = 64;        // single right-hand side: 1 consumer + 1 producer warp
 
 // Every sweep function is templated on K, the right-hand sides one consumer
@@ -76,6 +76,7 @@ __device__ __forceinline__ double ls_fetch(const double (&v)[R], int row_in_roun
 
 struct SweepCtx {
   const double* ring;  // smem ring base
+  int ns;              // ring stages in use
   uint64_t* full;
   uint64_t* empty;
   int stage_stride;    // doubles per stage
@@ -193,14 +194,15 @@ __device__ void ls_sweep(const SweepCtx& cx, int& chunk, int n, int kw, int stri
     for (int k = 0; k < K; ++k) nxt[k] = load_in(k, j0 + 32 * R + 32 + lane);
     // the round's records: one or two staged chunks
     const int nch = (min(32, n - j0) + LS_CH - 1) / LS_CH;
-    const int st0 = chunk % LS_NS;
-    if (!(dbg & 1)) mbar_wait(&cx.full[st0], (chunk / LS_NS) & 1);
+    // `chunk` = ring position as stage | parity << 8, advanced without a division (runtime ns)
+    const int st0 = chunk & 255, par0 = chunk >> 8;
+    if (!(dbg & 1)) mbar_wait(&cx.full[st0], par0);
     const double* rec0 = cx.ring + (size_t)st0 * cx.stage_stride;
     const double* rec1 = rec0;
     int st1 = st0;
     if (nch == 2) {
-      st1 = (chunk + 1) % LS_NS;
-      if (!(dbg & 1)) mbar_wait(&cx.full[st1], ((chunk + 1) / LS_NS) & 1);
+      st1 = st0 + 1 == cx.ns ? 0 : st0 + 1;
+      if (!(dbg & 1)) mbar_wait(&cx.full[st1], st1 == 0 ? par0 ^ 1 : par0);
       rec1 = cx.ring + (size_t)st1 * cx.stage_stride - LS_CH * stride;
     }
     // pivots of the round decoded once: lane s holds ipiv of step j0+s
@@ -224,7 +226,14 @@ __device__ void ls_sweep(const SweepCtx& cx, int& chunk, int n, int kw, int stri
       mbar_arrive(&cx.empty[st0]);
       if (nch == 2) mbar_arrive(&cx.empty[st1]);
     }
-    chunk += nch;
+    {
+      int st = st0 + nch, par = par0;
+      if (st >= cx.ns) {
+        st -= cx.ns;
+        par ^= 1;
+      }
+      chunk = st | (par << 8);
+    }
     const int row = j0 + lane;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -256,14 +265,14 @@ __device__ __forceinline__ void local_solve_body(const LocalDesc* __restrict__ d
                                                  const double* __restrict__ fwd, const double* __restrict__ bwd,
                                                  const double* __restrict__ r, double* __restrict__ xs,
                                                  int stage_stride, int dbg, long long ldr, long long xs_len,
-                                                 int nrhs) {
+                                                 int nrhs, int ns) {
   extern __shared__ __align__(128) double ring[];
   __shared__ __align__(8) uint64_t full[LS_NS], empty[LS_NS];
   const LocalDesc d = descs[blockIdx.x];
   const int nw = K == 1 ? 1 : (int)(blockDim.x >> 5) - 1;  // consumer warps
   const int warp = K == 1 ? (threadIdx.x >= 32 ? 1 : 0) : (int)(threadIdx.x >> 5);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < LS_NS; ++s) {
+    for (int s = 0; s < ns; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], nw);
     }
@@ -274,9 +283,13 @@ __device__ __forceinline__ void local_solve_body(const LocalDesc* __restrict__ d
   const int nc = (d.n + LS_CH - 1) / LS_CH;
   if (warp == nw) {
     if ((threadIdx.x & 31) == 0 && !(dbg & 1)) {  // producer
-      for (int c = 0; c < 2 * nc; ++c) {
-        const int stage = c % LS_NS;
-        if (c >= LS_NS) mbar_wait(&empty[stage], ((c / LS_NS) - 1) & 1);
+      int stage = 0, epar = 1;  // parity of the previous pass over the ring (none yet)
+      for (int c = 0; c < 2 * nc; ++c, ++stage) {
+        if (stage == ns) {
+          stage = 0;
+          epar ^= 1;
+        }
+        if (c >= ns) mbar_wait(&empty[stage], epar);
         const bool f = c < nc;
         const int cc = f ? c : c - nc;
         const int rows = min(LS_CH, d.n - cc * LS_CH);
@@ -289,7 +302,7 @@ __device__ __forceinline__ void local_solve_body(const LocalDesc* __restrict__ d
     }
     return;
   }
-  SweepCtx cx{ring, full, empty, stage_stride};
+  SweepCtx cx{ring, ns, full, empty, stage_stride};
   int chunk = 0;
   const int c0 = K == 1 ? 0 : warp * K;
   const int kc = K == 1 ? 1 : min(K, nrhs - c0);
@@ -314,20 +327,20 @@ __global__ void __launch_bounds__(LS_THREADS) k_local_solve(const LocalDesc* __r
                                                            const double* __restrict__ bwd,
                                                            const double* __restrict__ r, double* __restrict__ xs,
                                                            int stage_stride, int dbg, long long ldr,
-                                                           long long xs_len, int nrhs) {
-  local_solve_body<RF, RB, 1>(descs, idx, fwd, bwd, r, xs, stage_stride, dbg, ldr, xs_len, nrhs);
+                                                           long long xs_len, int nrhs, int ns) {
+  local_solve_body<RF, RB, 1>(descs, idx, fwd, bwd, r, xs, stage_stride, dbg, ldr, xs_len, nrhs, ns);
 }
 
 template <int RF, int RB>
 __global__ void __launch_bounds__(32 * (HG_MAX_RHS / LS_KM + 1), 2) k_local_solve_multi(
     const LocalDesc* __restrict__ descs, const int* __restrict__ idx, const double* __restrict__ fwd,
     const double* __restrict__ bwd, const double* __restrict__ r, double* __restrict__ xs, int stage_stride, int dbg,
-    long long ldr, long long xs_len, int nrhs) {
-  local_solve_body<RF, RB, LS_KM>(descs, idx, fwd, bwd, r, xs, stage_stride, dbg, ldr, xs_len, nrhs);
+    long long ldr, long long xs_len, int nrhs, int ns) {
+  local_solve_body<RF, RB, LS_KM>(descs, idx, fwd, bwd, r, xs, stage_stride, dbg, ldr, xs_len, nrhs, ns);
 }
 
 using LocalKernel = void (*)(const LocalDesc*, const int*, const double*, const double*, const double*,
-                             double*, int, int, long long, long long, int);
+                             double*, int, int, long long, long long, int, int);
 
 template <int RF, int RB, int NW>
 static LocalKernel pick2() {
@@ -387,12 +400,13 @@ static int launch_local_grid_t(HgPrecond* P, const LocalDesc* descs, int nblocks
     return HG_ERR_UNSUPPORTED;
   }
   const int stage_stride = LS_CH * (P->max_fstride > P->max_bstride ? P->max_fstride : P->max_bstride);
-  const size_t smem = (size_t)LS_NS * stage_stride * sizeof(double);
-  HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k), smem, false));
+  const int ns = P->ls_ns >= 2 && P->ls_ns <= LS_NS ? P->ls_ns : LS_NS;
+  const size_t smem = (size_t)ns * stage_stride * sizeof(double);
+  HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k), (size_t)LS_NS * stage_stride * sizeof(double), false));
   static const int dbg = getenv("HG_LOCAL_DEBUG") ? atoi(getenv("HG_LOCAL_DEBUG")) : 0;  // timing experiments only
   const int nwarps = NW == 1 ? 1 : (nrhs + LS_KM - 1) / LS_KM;  // consumer warps
   k<<<nblocks, 32 * (nwarps + 1), smem, st>>>(descs, P->d_local_idx, P->d_fwd, P->d_bwd, r, xs ? xs : P->d_xs,
-                                               stage_stride, dbg, ldr, xs_len, nrhs);
+                                               stage_stride, dbg, ldr, xs_len, nrhs, ns);
   HG_LAUNCH_CHECK();
   return HG_OK;
 }

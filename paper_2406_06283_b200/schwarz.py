@@ -429,8 +429,30 @@ class TwoLevelPreconditioner:
         self.setup_times["create"] = self._t() - t0
         if self.m:
             t0 = self._t()
+            if meta.get("b0_split"):
+                # the bisected coarse solve against getrs first; beyond the bar it is switched off
+                # (and leaves the image), and the full chain is checked as before
+                meta["b0_split_dev"] = self._check_coarse_solve(strict=False)
+                if not meta["b0_split_dev"] <= 1e-11:
+                    _lib.check(_lib.load().hg_debug_set(self._handle, _lib.DEBUG_B0_SPLIT, 0), "hg_debug_set")
+                    meta["b0_split"] = 0
+                    arrays = {k: v for k, v in arrays.items() if k not in self.B0_SPLIT_KEYS}
+            self.b0_split = bool(meta.get("b0_split"))
+            if self.b0_split:
+                # the full chain too (the bisected one can be switched off: the tuning below, tests)
+                self._set_tune(b0_split_on=False)
             meta["b0_tile_dev"] = self.b0_tile_dev = self._check_coarse_solve()
             self.setup_times["b0_guard"] = self._t() - t0
+            if self.b0_split:
+                t0 = self._t()
+                if os.environ.get("HG_B0_SPLIT", "auto") == "1":  # forced: no timing
+                    meta["tune"] = {"b0_split_on": True, "local_stages": int(os.environ.get("HG_LOCAL_STAGES", "0"))}
+                    self._set_tune(b0_split_on=True, local_stages=meta["tune"]["local_stages"])
+                else:
+                    meta["tune"] = self._tune_single_apply()
+                if meta["tune"]["b0_split_on"] and (not meta.get("b0_dense") or meta.get("b0_inv_batched_only")):
+                    meta["b0_bytes"] = self.b0_bytes = int(meta["b0_bytes_split"])
+                self.setup_times["apply_tuning"] = self._t() - t0
         if "b0_inv" in arrays and not isinstance(arrays["b0_inv"], np.ndarray):  # device copy: host only if cached
             arrays = dict(arrays)
             binv = arrays.pop("b0_inv")
@@ -643,6 +665,11 @@ class TwoLevelPreconditioner:
                     if dense != "multi":
                         M["b0_bytes"] = int(8 * m * m + 16 * m)
             self.setup_times["b0_inverse"] = self._t() - t0
+            M["b0_split"] = 0
+            if mode == 1 and not host_only and os.environ.get("HG_B0_SPLIT", "auto") != "0":
+                t0 = self._t()
+                self._b0_bisection(A, M, cs)
+                self.setup_times["b0_bisection"] = self._t() - t0
             M["n_cblk"] = len(cblocks)
             put("cblk_n", [i.size for i, _ in cblocks], i32)
             put("cblk_m", [b.shape[1] for _, b in cblocks], i32)
@@ -734,6 +761,119 @@ class TwoLevelPreconditioner:
         M["split_chunks"] = int(max(len(sb.chunks) for _, sb, _ in splits))
         M["split_cond"] = float(max(sb.cond for _, sb, _ in splits))
 
+    def _b0_bisection(self, A, M, cs):
+        """Descriptor arrays of the bisected single-RHS coarse solve (helmgpu.h
+        "Bisected coarse solve"): B0 is banded, so two half chains + a dense
+        separator system replace one chain of 2K hand-offs.  Built on the
+        device (torch.linalg, setup only); declined when B0 is short
+        (K < 96 panels unless HG_B0_SPLIT=1) or the halves' tile rings do not
+        fit.  The caller checks the result against getrs (_check_coarse_solve)."""
+        torch = _torch()
+        B0 = np.ascontiguousarray(np.asarray(self._coarse.B0), dtype=np.float64)
+        m = B0.shape[0]
+        if os.environ.get("HG_B0_SPLIT", "auto") != "1" and (m + 63) // 64 < 96:
+            return
+        bw = 0
+        for r0 in range(0, m, 1024):
+            rr, cc = np.nonzero(B0[r0:r0 + 1024])
+            if rr.size:
+                bw = max(bw, int(np.abs(cc - (rr + r0)).max()))
+        ns = max(bw, 1)
+        forced = os.environ.get("HG_B0_SPLIT", "auto") == "1"
+        if m - ns < (2 if forced else 8) * ns:  # halves shorter than the separator (than 4 of them): not worth it
+            return
+        a = (m - ns) // 2
+        wl, wr = min(bw, a), min(bw, m - a - ns)
+        Bd = torch.from_numpy(B0).cuda()
+        S = slice(a, a + ns)
+        sig = Bd[S, S].clone()
+        halves, Ws = [], []
+        for h in (slice(0, a), slice(a + ns, m)):
+            Ah = Bd[h, h].contiguous()
+            LU, piv = torch.linalg.lu_factor(Ah)
+            E = Bd[h, S].contiguous()
+            W = torch.linalg.lu_solve(LU, piv, E)
+            W = W + torch.linalg.lu_solve(LU, piv, E - Ah @ W)  # one refinement step
+            sig -= Bd[S, h] @ W
+            Ws.append(W)
+            T = pack_b0_tiles(LU.cpu().numpy(), piv.cpu().numpy().astype(np.int64) - 1, 64)
+            # a full cluster per half chain (8 CTAs stream a half's tiles too slowly: 0.58 vs 0.37 ms)
+            c = min(int(os.environ.get("HG_B0_SPLIT_CS", cs)), T.K)
+            ring = tile_span(T) + c + 1
+            if ring > 96:
+                return
+            halves.append((T.premultiply(), c, ring))
+            del Ah, LU, E
+        sinv = torch.linalg.inv(sig)
+        F = torch.cat([Bd[S, a - wl:a], Bd[S, a + ns:a + ns + wr]], dim=1).contiguous()
+        f64, i32, i64 = np.float64, np.int32, np.int64
+        M["b0_split"] = 1
+        M["b0s_a"], M["b0s_ns"], M["b0s_wl"], M["b0s_wr"] = int(a), int(ns), int(wl), int(wr)
+        nbytes = 0
+        for h, (T, c, ring) in enumerate(halves):
+            pre = "b0h%d_" % h
+            M[pre + "npanel"], M[pre + "ring"], M[pre + "cluster"] = int(T.K), int(ring), int(c)
+            M[pre + "ntile"] = int(T.tile_col.size)
+            A[pre + "perm"] = np.ascontiguousarray(T.perm, dtype=i32)
+            A[pre + "dinv"] = np.ascontiguousarray(swizzle_tile_rows(T.dinv), dtype=f64)
+            A[pre + "tile_ptr"] = np.ascontiguousarray(T.tile_ptr, dtype=i64)
+            A[pre + "tile_col"] = np.ascontiguousarray(T.tile_col if T.tile_col.size else np.zeros(1), dtype=i32)
+            A[pre + "tiles"] = np.ascontiguousarray(swizzle_tile_rows(T.tiles) if T.tiles.size else np.zeros(1),
+                                                    dtype=f64)
+            nbytes += T.nbytes + 4 * T.perm.size
+        A["b0s_f"] = F.cpu().numpy()
+        A["b0s_sinv"] = sinv.contiguous().cpu().numpy()
+        A["b0s_w"] = torch.cat(Ws, dim=0).contiguous().cpu().numpy()
+        nbytes += A["b0s_f"].nbytes + A["b0s_sinv"].nbytes + A["b0s_w"].nbytes
+        M["b0_bytes_chain"] = int(M["b0_bytes"])
+        M["b0_bytes_split"] = int(nbytes)
+
+    B0_SPLIT_KEYS = ("b0h0_perm", "b0h0_dinv", "b0h0_tile_ptr", "b0h0_tile_col", "b0h0_tiles", "b0h1_perm",
+                     "b0h1_dinv", "b0h1_tile_ptr", "b0h1_tile_col", "b0h1_tiles", "b0s_f", "b0s_sinv", "b0s_w")
+
+    def _set_tune(self, b0_split_on=None, local_stages=None):
+        lib = _lib.load()
+        if b0_split_on is not None:
+            _lib.check(lib.hg_debug_set(self._handle, _lib.DEBUG_B0_SPLIT, 1 if b0_split_on else 0), "hg_debug_set")
+        if local_stages is not None:
+            _lib.check(lib.hg_debug_set(self._handle, _lib.DEBUG_LOCAL_STAGES, int(local_stages)), "hg_debug_set")
+
+    def _tune_single_apply(self):
+        """Which single-RHS apply schedule this handle runs: the bisected coarse
+        solve holds two clusters (32 SMs) instead of one, which only pays when
+        the local solves' CTAs still fit beside them in one wave — with 4 ring
+        stages instead of 6 where that takes a third CTA per SM.  Decided by
+        timing the apply itself (device events, 3 + 12 applies per candidate);
+        the default schedule (full chain, 6 stages) stays unless another one is
+        at least 8% faster, so that near-ties never flip between runs.  The
+        choice is part of the image (the setup cache reproduces it)."""
+        torch = _torch()
+        r = torch.from_numpy(np.random.default_rng(7).standard_normal(self.n)).cuda()
+
+        def timed():
+            for _ in range(3):
+                self.apply(r)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(torch.cuda.current_stream())
+            for _ in range(12):
+                self.apply(r)
+            e1.record(torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / 12
+
+        cands = [(False, 0), (True, 0), (True, 4)]
+        ms = {}
+        for split_on, stages in cands:
+            self._set_tune(b0_split_on=split_on, local_stages=stages)
+            ms[(split_on, stages)] = timed()
+        best = min(ms, key=ms.get)
+        if ms[best] > 0.92 * ms[(False, 0)]:
+            best = (False, 0)
+        self._set_tune(b0_split_on=best[0], local_stages=best[1])
+        return {"b0_split_on": bool(best[0]), "local_stages": int(best[1]),
+                "apply_ms": {"%s,%d" % ("bisected" if k[0] else "chain", k[1] or 6): round(v, 4) for k, v in ms.items()}}
+
     def _getrs(self):
         """c -> getrs(lu, piv, c) (the reference's lu_solve, schwarz.py:56) with the
         same getrf factors; on the device when there is one (the factors are
@@ -754,7 +894,7 @@ class TwoLevelPreconditioner:
         self._getrs_fn = fn
         return fn
 
-    def _tile_guard(self, solve, m, P):
+    def _tile_guard(self, solve, m, P, strict=True):
         """Max relative deviation of a B0 solve from getrs on 4 seeded vectors;
         raises SingularOperatorError above 1e-11 (B0 too ill-conditioned for the
         inverted diagonal blocks of the tile algorithm)."""
@@ -765,13 +905,13 @@ class TwoLevelPreconditioner:
             c = rng.standard_normal(m)
             want = getrs(c)
             dev = max(dev, float(np.abs(solve(c) - want).max() / max(np.abs(want).max(), 1e-300)))
-        if dev > 1e-11:
+        if dev > 1e-11 and strict:
             raise SingularOperatorError(
                 "coarse tile factorisation deviates from getrs by %.2e (B0 too ill-conditioned for "
                 "inverted %dx%d diagonal blocks)" % (dev, P, P))
         return dev
 
-    def _check_coarse_solve(self):
+    def _check_coarse_solve(self, strict=True):
         """The guard of the tiled coarse solve, run on the device chain kernel itself."""
         torch = _torch()
 
@@ -782,8 +922,9 @@ class TwoLevelPreconditioner:
                        "hg_precond_coarse_solve")
             return y.cpu().numpy()
 
-        res = self._tile_guard(dev_solve, self.m, self.b0_tiles.P)
-        self._getrs_fn = None  # the device copy of the factors is not kept
+        res = self._tile_guard(dev_solve, self.m, self.b0_tiles.P, strict)
+        if strict:
+            self._getrs_fn = None  # the device copy of the factors is not kept
         return res
 
     def _create(self, arrays, meta):
@@ -807,6 +948,9 @@ class TwoLevelPreconditioner:
         self._handle = h
         self._meta = meta
         self.m = int(meta["m"])
+        tune = meta.get("tune")
+        if tune and meta.get("b0_split"):  # a cached image: the schedule its setup chose
+            self._set_tune(b0_split_on=tune["b0_split_on"], local_stages=tune["local_stages"])
         self.local_sizes = [int(x) for x in arrays["local_n"]] if "local_n" in arrays else []
         self.xs_len = int(np.asarray(arrays["local_idx_off"])[-1]) if "local_idx_off" in arrays else 0
         self.local_bands = [tuple(b) for b in meta["local_bands"]]
@@ -817,6 +961,7 @@ class TwoLevelPreconditioner:
         self.b0_dense = bool(meta["b0_dense"])
         self.b0_dense_dev = meta.get("b0_dense_dev")
         self.b0_tile_dev = meta.get("b0_tile_dev")
+        self.b0_split = bool(meta.get("b0_split"))
         self.split_bytes = int(meta.get("split_bytes", 0))
         self.n_split = int(meta.get("n_split", 0))
         self.panel_active = bool(lib.hg_precond_stat(h, _lib.STAT_PANEL_ACTIVE) == 1.0)
