@@ -472,10 +472,14 @@ def run_ours(args, dist):
         dist.barrier()
         e0.record(stream)
         it_e2e = 0
+        t_steps = []
         for s in range(args.steps):
+            t_s = time.perf_counter()
             X, reps = pre.solve_host_batch(Fh, rtol=rtol, maxit=maxit)
+            t_steps.append(round((time.perf_counter() - t_s) * 1e3, 1))
             it_e2e += sum(r.iterations for r in reps)
         e1.record(stream)
+        log("e2e steps (host ms): %s" % t_steps)
         torch.cuda.synchronize()
         ms_e2e = dist.max(e0.elapsed_time(e1))
         e2e = {"value": round(dist.sum(it_e2e) / (ms_e2e / 1e3), 3), "unit": "iters/s",
