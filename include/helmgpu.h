@@ -444,6 +444,8 @@ int64_t hg_dcgs2_explicit_passes(void);
 /* ring stages of the single-RHS local solve (4..6; fewer stages = less shared memory = more CTAs
  * per SM beside the coarse chains) */
 #define HG_DEBUG_LOCAL_STAGES 5
+/* tile ring stages of the cluster coarse chain (2..4; 2 leaves room for a local-solve CTA on its SMs) */
+#define HG_DEBUG_B0_TILE_STAGES 6
 int hg_debug_set(HgPrecond* p, int32_t key, int64_t value);
 
 /* Krylov basis of the last hg_gmres / hg_gmres_batch solve on `op`

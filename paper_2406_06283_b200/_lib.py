@@ -183,6 +183,7 @@ FIELD_LOCAL_FWD, FIELD_LOCAL_BWD = 1, 2
 
 ABI_VERSION = 5
 DEBUG_SPIN_LIMIT_MS, DEBUG_SKIP_ZT, DEBUG_FORCE_EXPLICIT_RHO, DEBUG_B0_SPLIT, DEBUG_LOCAL_STAGES = 1, 2, 3, 4, 5
+DEBUG_B0_TILE_STAGES = 6
 MAX_BASIS = 1024  # Krylov vectors the basis kernels support (MAX_NV)
 NPHASES = 7  # HG_NPHASES
 ORTH = {"measured": 0, "dcgs2": 1}

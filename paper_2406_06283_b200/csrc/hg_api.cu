@@ -52,6 +52,10 @@ int ensure_func_attrs(const void* func, size_t smem, bool nonportable_cluster) {
   if (have >= smem && have != 0) return HG_OK;
   HG_CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (nonportable_cluster) HG_CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  // kernels built around a shared-memory ring ask for the largest carve-out, so that CTAs of two such
+  // kernels (a coarse chain and a local solve) can share an SM whenever their rings fit together
+  if (smem >= 64 * 1024)
+    HG_CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared));
   have = smem > 0 ? smem : 1;
   return HG_OK;
 }
@@ -1385,6 +1389,14 @@ int hg_debug_set(HgPrecond* P, int32_t key, int64_t value) {
         return HG_ERR_ARG;
       }
       P->ls_ns = (int)value;
+      return HG_OK;
+    case HG_DEBUG_B0_TILE_STAGES:
+      if (!P) break;
+      if (value != 0 && (value < 2 || value > 4)) {
+        set_error("hg_debug_set: tile stages must be 0 (default) or 2..4");
+        return HG_ERR_ARG;
+      }
+      P->b0_tns = (int)value;
       return HG_OK;
     case HG_DEBUG_B0_SPLIT: {
       if (!P) break;

@@ -47,7 +47,7 @@ namespace {
 constexpr int CP = 64;             // panel size
 constexpr int CONS = 256;          // consumer threads (64 rows x 4)
 constexpr int CTHREADS = CONS + 32;
-constexpr int TNS = 4;             // tile ring stages
+constexpr int TNS = 4;             // tile ring stages at most (runtime count B0ClusterArgs::tns, 2..4)
 constexpr int TILE_DOUBLES = CP * CP;
 
 __device__ __forceinline__ uint32_t mapa(uint32_t smem_addr, uint32_t rank) {
@@ -146,6 +146,7 @@ __device__ __forceinline__ double row_dot(const double* trow, int row, int q, co
 
 struct B0ClusterArgs {
   int m, K, NR, CS;
+  int tns;                  // tile ring stages (fewer = less shared memory: a local-solve CTA fits beside)
   const int* perm;
   const int* col_blk;
   const CblkDesc* descs;
@@ -165,7 +166,8 @@ struct B0ClusterArgs {
 __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
   extern __shared__ __align__(128) double sm[];
   double* tring = sm;                                   // TNS x TILE_DOUBLES
-  double* xring = tring + (size_t)TNS * TILE_DOUBLES;   // NR x CP (value, tag) pairs
+  const int tns = a.tns;
+  double* xring = tring + (size_t)tns * TILE_DOUBLES;   // NR x CP (value, tag) pairs
   double* rhs = xring + (size_t)a.NR * CP * 2;          // CP
   uint64_t* tfull = reinterpret_cast<uint64_t*>(rhs + CP);
   uint64_t* tempty = tfull + TNS;
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
   for (int i = tid; i < NR * CP; i += CTHREADS) xring[2 * i + 1] = -1.0;  // no panel yet
   if (tid == 0) {
     s_launch = take_launch_index(a.ticket, CS);
-    for (int s = 0; s < TNS; ++s) {
+    for (int s = 0; s < tns; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], CONS / 32);
     }
@@ -191,12 +193,15 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
   if (tid >= CONS) {
     // ---- producer warp: per own panel, the inverse block then the tiles
     if (tid == CONS) {
-      int c = 0;
+      int c = 0, stage = 0, epar = 1;  // epar: parity of the previous pass over the ring
       for (int g = rank; g < 2 * K; g += CS) {
         const long long e0 = a.tile_ptr[g], e1 = a.tile_ptr[g + 1];
-        for (long long e = e0 - 1; e < e1; ++e, ++c) {  // e == e0 - 1: the inverse block
-          const int stage = c % TNS;
-          if (c >= TNS) mbar_wait(&tempty[stage], ((c / TNS) - 1) & 1);
+        for (long long e = e0 - 1; e < e1; ++e, ++c, ++stage) {  // e == e0 - 1: the inverse block
+          if (stage == tns) {
+            stage = 0;
+            epar ^= 1;
+          }
+          if (c >= tns) mbar_wait(&tempty[stage], epar);
           const double* src = (e < e0) ? a.dinv + (size_t)g * TILE_DOUBLES : a.tiles + (size_t)e * TILE_DOUBLES;
           mbar_arrive_expect_tx(&tfull[stage], TILE_DOUBLES * 8u);
           bulk_g2s(tring + (size_t)stage * TILE_DOUBLES, src, TILE_DOUBLES * 8u, &tfull[stage]);
@@ -206,7 +211,13 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
   } else {
     // ---- consumers: 64 rows x 4 threads; thread q owns chunks q + 4k (k = 0..7)
     const int row = tid >> 2, q = tid & 3, lane = tid & 31;
-    int c = 0;  // tile-stream position
+    int stage = 0, fpar = 0;  // tile-stream position: ring stage and its parity (no division: runtime tns)
+    auto next_tile = [&]() {
+      if (++stage == tns) {
+        stage = 0;
+        fpar ^= 1;
+      }
+    };
     bool l_done = false;
     bool dead = false;  // a bounded wait gave up: finish on garbage, the host reports the fault
     const unsigned long long zt_launches = s_launch + 1;
@@ -251,15 +262,14 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
           xv[2 * k + 1] = r2.y;
         }
       }
-      int stage = c % TNS;
-      mbar_wait(&tfull[stage], (c / TNS) & 1);
+      mbar_wait(&tfull[stage], fpar);
       double acc = row_dot(tring + (size_t)stage * TILE_DOUBLES + row * CP, row, q, xv);  // D_t^{-1} rhs_t
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[stage]);
-      ++c;
+      next_tile();
       const long long e0 = a.tile_ptr[g], e1 = a.tile_ptr[g + 1];
       bool saw_prev = (g == 0) || (ph == 1 && t == 0);
-      for (long long e = e0; e < e1; ++e, ++c) {
+      for (long long e = e0; e < e1; ++e, next_tile()) {
         const int gj = ph * K + a.tile_col[e];
         if (stamp && gj == g - 1) g_b0c_stamps[4 * g + 1] = gtimer_b0c();
         poll_panel(xring, gj, NR, q, xv, a.spin, dead);
@@ -267,8 +277,7 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
           saw_prev = true;
           if (stamp) g_b0c_stamps[4 * g + 2] = gtimer_b0c();
         }
-        stage = c % TNS;
-        mbar_wait(&tfull[stage], (c / TNS) & 1);
+        mbar_wait(&tfull[stage], fpar);
         acc -= row_dot(tring + (size_t)stage * TILE_DOUBLES + row * CP, row, q, xv);
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[stage]);
@@ -309,14 +318,14 @@ __global__ void __launch_bounds__(CTHREADS, 1) k_b0_cluster(B0ClusterArgs a) {
   cluster_sync_all();
 }
 
-size_t b0_cluster_smem(int NR) {
-  return sizeof(double) * ((size_t)TNS * TILE_DOUBLES + (size_t)NR * CP * 2 + CP) +
+size_t b0_cluster_smem(int NR, int tns) {
+  return sizeof(double) * ((size_t)tns * TILE_DOUBLES + (size_t)NR * CP * 2 + CP) +
          sizeof(uint64_t) * (2 * TNS + 1);
 }
 
 static int launch_chain(const B0ClusterArgs& a, cudaStream_t st) {
-  const size_t smem = b0_cluster_smem(a.NR);
-  HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k_b0_cluster), smem, true));
+  const size_t smem = b0_cluster_smem(a.NR, a.tns);
+  HG_TRY(ensure_func_attrs(reinterpret_cast<const void*>(k_b0_cluster), b0_cluster_smem(a.NR, TNS), true));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.CS);
   cfg.blockDim = dim3(CTHREADS);
@@ -388,7 +397,8 @@ __global__ void __launch_bounds__(256) k_b0s_w(int m, int ns, int a, const doubl
 
 static B0ClusterArgs half_args(HgPrecond* P, int h) {
   const HgPrecond::B0Half& c = P->b0h[h];
-  return B0ClusterArgs{c.m, c.K, c.nr, c.cs, c.perm, P->d_col_blk, P->d_cblk, P->d_cpart, c.dinv,
+  const int tns = P->b0_tns >= 2 && P->b0_tns <= TNS ? P->b0_tns : TNS;
+  return B0ClusterArgs{c.m, c.K, c.nr, c.cs, tns, c.perm, P->d_col_blk, P->d_cblk, P->d_cpart, c.dinv,
                        c.tile_ptr, c.tile_col, c.tiles, c.xbuf, P->d_y + c.off,
                        P->d_blk_done, P->d_ticket + 2 + h, spin_cfg(P)};
 }
@@ -424,7 +434,8 @@ int launch_coarse_solve_cluster(HgPrecond* P, cudaStream_t st) {
   }
   const int K = P->b0_K;
   const int CS = P->b0_cs;
-  B0ClusterArgs a{P->m, K, P->b0_nr, CS, P->d_b0_perm, P->d_col_blk, P->d_cblk, P->d_cpart, P->d_b0_dinv,
+  const int tns = P->b0_tns >= 2 && P->b0_tns <= TNS ? P->b0_tns : TNS;
+  B0ClusterArgs a{P->m, K, P->b0_nr, CS, tns, P->d_b0_perm, P->d_col_blk, P->d_cblk, P->d_cpart, P->d_b0_dinv,
                   P->d_b0_tile_ptr, P->d_b0_tile_col, P->d_b0_tiles, P->d_b0_x, P->d_y,
                   P->d_blk_done, P->d_ticket, spin_cfg(P)};
   HG_TRY(launch_chain(a, st));

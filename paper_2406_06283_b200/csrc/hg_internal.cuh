@@ -102,6 +102,7 @@ struct HgPrecond {
   };
   bool b0_split = false;            // bisected data present
   bool b0_split_on = false;         // ... and in use (hg_debug_set can switch it off)
+  int b0_tns = 0;                   // tile ring stages of the chain kernel (0 = the default 4; hg_debug_set)
   B0Half b0h[2];
   int b0s_a = 0, b0s_ns = 0, b0s_wl = 0, b0s_wr = 0;
   double* d_b0s_f = nullptr;
@@ -256,7 +257,7 @@ int launch_coarse_sep_split(HgPrecond* P, cudaStream_t st);
 SpinCfg spin_cfg(const HgPrecond* P);
 // per (kernel, device) dynamic shared memory / cluster attributes (thread safe)
 int ensure_func_attrs(const void* func, size_t smem, bool nonportable_cluster);
-size_t b0_cluster_smem(int NR);
+size_t b0_cluster_smem(int NR, int tns = 4);
 // force-load kernels at handle creation (see preload_local in hg_local.cu)
 int preload_local(HgPrecond* P);
 int preload_local_multi(HgPrecond* P);

@@ -446,8 +446,10 @@ class TwoLevelPreconditioner:
             if self.b0_split:
                 t0 = self._t()
                 if os.environ.get("HG_B0_SPLIT", "auto") == "1":  # forced: no timing
-                    meta["tune"] = {"b0_split_on": True, "local_stages": int(os.environ.get("HG_LOCAL_STAGES", "0"))}
-                    self._set_tune(b0_split_on=True, local_stages=meta["tune"]["local_stages"])
+                    meta["tune"] = {"b0_split_on": True, "local_stages": int(os.environ.get("HG_LOCAL_STAGES", "0")),
+                                    "b0_tile_stages": int(os.environ.get("HG_B0_TILE_STAGES", "0"))}
+                    self._set_tune(b0_split_on=True, local_stages=meta["tune"]["local_stages"],
+                                   tile_stages=meta["tune"]["b0_tile_stages"])
                 else:
                     meta["tune"] = self._tune_single_apply()
                 if meta["tune"]["b0_split_on"] and (not meta.get("b0_dense") or meta.get("b0_inv_batched_only")):
@@ -831,8 +833,10 @@ class TwoLevelPreconditioner:
     B0_SPLIT_KEYS = ("b0h0_perm", "b0h0_dinv", "b0h0_tile_ptr", "b0h0_tile_col", "b0h0_tiles", "b0h1_perm",
                      "b0h1_dinv", "b0h1_tile_ptr", "b0h1_tile_col", "b0h1_tiles", "b0s_f", "b0s_sinv", "b0s_w")
 
-    def _set_tune(self, b0_split_on=None, local_stages=None):
+    def _set_tune(self, b0_split_on=None, local_stages=None, tile_stages=None):
         lib = _lib.load()
+        if tile_stages is not None:
+            _lib.check(lib.hg_debug_set(self._handle, _lib.DEBUG_B0_TILE_STAGES, int(tile_stages)), "hg_debug_set")
         if b0_split_on is not None:
             _lib.check(lib.hg_debug_set(self._handle, _lib.DEBUG_B0_SPLIT, 1 if b0_split_on else 0), "hg_debug_set")
         if local_stages is not None:
@@ -862,17 +866,20 @@ class TwoLevelPreconditioner:
             torch.cuda.synchronize()
             return e0.elapsed_time(e1) / 12
 
-        cands = [(False, 0), (True, 0), (True, 4)]
+        # (bisected?, local ring stages, coarse tile-ring stages; 0 = default): fewer stages = less shared
+        # memory per CTA, i.e. a third local CTA per SM / a local CTA on the chains' SMs
+        cands = [(False, 0, 0), (True, 0, 0), (True, 4, 0), (True, 0, 2), (True, 4, 2)]
         ms = {}
-        for split_on, stages in cands:
-            self._set_tune(b0_split_on=split_on, local_stages=stages)
-            ms[(split_on, stages)] = timed()
+        for cand in cands:
+            self._set_tune(b0_split_on=cand[0], local_stages=cand[1], tile_stages=cand[2])
+            ms[cand] = timed()
         best = min(ms, key=ms.get)
-        if ms[best] > 0.92 * ms[(False, 0)]:
-            best = (False, 0)
-        self._set_tune(b0_split_on=best[0], local_stages=best[1])
-        return {"b0_split_on": bool(best[0]), "local_stages": int(best[1]),
-                "apply_ms": {"%s,%d" % ("bisected" if k[0] else "chain", k[1] or 6): round(v, 4) for k, v in ms.items()}}
+        if ms[best] > 0.92 * ms[cands[0]]:
+            best = cands[0]
+        self._set_tune(b0_split_on=best[0], local_stages=best[1], tile_stages=best[2])
+        return {"b0_split_on": bool(best[0]), "local_stages": int(best[1]), "b0_tile_stages": int(best[2]),
+                "apply_ms": {"%s,%d,%d" % ("bisected" if k[0] else "chain", k[1] or 6, k[2] or 4): round(v, 4)
+                             for k, v in ms.items()}}
 
     def _getrs(self):
         """c -> getrs(lu, piv, c) (the reference's lu_solve, schwarz.py:56) with the
@@ -950,7 +957,8 @@ class TwoLevelPreconditioner:
         self.m = int(meta["m"])
         tune = meta.get("tune")
         if tune and meta.get("b0_split"):  # a cached image: the schedule its setup chose
-            self._set_tune(b0_split_on=tune["b0_split_on"], local_stages=tune["local_stages"])
+            self._set_tune(b0_split_on=tune["b0_split_on"], local_stages=tune["local_stages"],
+                           tile_stages=tune.get("b0_tile_stages", 0))
         self.local_sizes = [int(x) for x in arrays["local_n"]] if "local_n" in arrays else []
         self.xs_len = int(np.asarray(arrays["local_idx_off"])[-1]) if "local_idx_off" in arrays else 0
         self.local_bands = [tuple(b) for b in meta["local_bands"]]
