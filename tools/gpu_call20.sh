@@ -1,0 +1,5 @@
+set -x
+python -m pytest tests -m gpu -x -q > gpurun_out/r2e_pytest_all.log 2>&1; tail -4 gpurun_out/r2e_pytest_all.log
+python bench.py > gpurun_out/r2e_bench_5-16.json 2> gpurun_out/r2e_bench_5-16.err; tail -3 gpurun_out/r2e_bench_5-16.err
+python bench.py --config 5-8 --no-cpu-baseline > gpurun_out/r2e_bench_5-8.json 2> gpurun_out/r2e_bench_5-8.err; tail -2 gpurun_out/r2e_bench_5-8.err
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
