@@ -96,3 +96,28 @@ def test_split_cache_round_trip(cfg3, monkeypatch, tmp_path):
     assert np.array_equal(pre.apply(r), again.apply(r))
     R = np.random.default_rng(6).standard_normal((pre.n, 16))
     assert np.array_equal(pre.apply_multi(R), again.apply_multi(R))
+
+
+def test_inconsistent_split_descriptors_are_refused(monkeypatch):
+    """hg_precond_create validates the split-block description (helmgpu.h): positions out of the
+    solution scratch, a split that does not name a separator pseudo block, a spike past its data."""
+    from paper_2406_06283_b200 import schwarz
+    from paper_2406_06283_b200.schwarz import TwoLevelPreconditioner
+
+    P = hg.build_problem("1", workers=1, one_level=True)
+    monkeypatch.setenv("HG_LOCAL_SPLIT", "2")
+    A, M = schwarz.host_image(P.forms, P.dec, None)
+    assert M["n_split"] > 0
+    good = TwoLevelPreconditioner.from_image(dict(A), dict(M))
+    r = np.random.default_rng(1).standard_normal(good.n)
+    assert np.isfinite(good.apply(r)).all()
+
+    def broken(name, mutate):
+        arrays = {k: np.array(v, copy=True) for k, v in A.items()}
+        mutate(arrays)
+        with pytest.raises(hg.DeviceError, match=name):
+            TwoLevelPreconditioner.from_image(arrays, dict(M))
+
+    broken("position out of range", lambda a: a["split_f_pos"].__setitem__(0, int(a["local_idx_off"][-1]) + 5))
+    broken("pseudo block", lambda a: a["split_blk"].__setitem__(0, 0))
+    broken("spike", lambda a: a["spike_off"].__setitem__(len(a["spike_off"]) - 1, int(M["spike_len"])))
