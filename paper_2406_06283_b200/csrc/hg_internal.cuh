@@ -173,7 +173,7 @@ struct HgPrecond {
   double* d_ztpk = nullptr;
   long long* d_zypk_off = nullptr;
   long long* d_ztpk_off = nullptr;
-  int2* d_zy_items = nullptr;     // (block, pair of 8-row tiles)
+  void* d_zy_items = nullptr;     // ZyItem per pair of 8-row tiles (hg_multi.cu)
   int n_zy_items = 0;
   double* d_b0m_x = nullptr;      // [2][K*64][HG_MAX_RHS] phase solutions
   double* d_tmpm = nullptr;       // [c][n] scratch (B U for the batched apply_T)

@@ -123,8 +123,8 @@ int launch_spmm_self(const DevCsr& A, const double* vals, const double* X, long 
 // ------------------------------------------------------------------ Z^T R
 __global__ void k_zt_multi_pk(const int2*, const CblkDesc*, const int*, const long long*, const double2*, const double*,
                               long long, int, double*, unsigned long long*);
-__global__ void k_zy_multi_pk(const int2*, int, const CblkDesc*, const long long*, const double2*, const double*, int,
-                              double*, long long);
+struct ZyItem;
+__global__ void k_zy_multi_pk(const ZyItem*, int, const double2*, const double*, int, double*, long long);
 __global__ void __launch_bounds__(256) k_zt_multi(const int2* __restrict__ items, const CblkDesc* __restrict__ descs,
                                                   const int* __restrict__ idx, const double* __restrict__ Z,
                                                   const double* __restrict__ R, long long ldr, int nrhs,
@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(256) k_zy_multi(const int2* __restrict__ items
 int launch_zy_multi(HgPrecond* P, int nrhs, cudaStream_t st) {
   if (P->m == 0 || P->n_zt_items == 0) return HG_OK;
   if (P->d_zypk)
-    k_zy_multi_pk<<<ceil_div(P->n_zy_items, 8), 256, 0, st>>>(P->d_zy_items, P->n_zy_items, P->d_cblk, P->d_zypk_off,
+    k_zy_multi_pk<<<ceil_div(P->n_zy_items, 8), 256, 0, st>>>(reinterpret_cast<const ZyItem*>(P->d_zy_items),
+                                                               P->n_zy_items,
                                                                reinterpret_cast<const double2*>(P->d_zypk), P->d_ym,
                                                                nrhs, P->d_zsm, P->zs_len);
   else
@@ -341,23 +342,27 @@ __global__ void __launch_bounds__(256) k_zt_multi_pk(const int2* __restrict__ it
 }
 
 // U_b rows: a warp owns two 8-row tiles of a block and streams their packed fragments (at most
-// 2 x 8 loads, all issued before the first product); Y comes from [coarse column][16] through L1
-__global__ void __launch_bounds__(256) k_zy_multi_pk(const int2* __restrict__ items, int nitems,
-                                                     const CblkDesc* __restrict__ descs,
-                                                     const long long* __restrict__ zoff,
+// 2 x 8 loads, all issued before the first product); Y comes from [coarse column][16] through L1.
+// The work item carries everything the warp needs (no dependent descriptor loads before the stream).
+struct ZyItem {
+  long long a_off;    // double2 index of the pair's first packed tile
+  long long dst_off;  // position of the pair's first row in the zs scratch
+  int col0, m;        // the block's first coarse column and its width
+  int rows, pad;      // rows of the pair that exist (1..16)
+};
+
+__global__ void __launch_bounds__(256) k_zy_multi_pk(const ZyItem* __restrict__ items, int nitems,
                                                      const double2* __restrict__ zp, const double* __restrict__ ym,
                                                      int nrhs, double* __restrict__ zsm, long long zs_len) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, g = lane >> 2;
   const int iw = blockIdx.x * 8 + warp;
   if (iw >= nitems) return;
-  const int2 it = items[iw];
-  const CblkDesc d = descs[it.x];
-  const int KB = (d.m + 7) >> 3, MT = (d.n + 7) >> 3;
-  const int mt0 = it.y * 2;
-  const bool two = mt0 + 1 < MT;
-  const double2* a0p = zp + (zoff[it.x] >> 1) + (size_t)mt0 * KB * 32 + lane;
+  const ZyItem it = items[iw];
+  const int KB = (it.m + 7) >> 3;
+  const bool two = it.rows > 8;
+  const double2* a0p = zp + it.a_off + lane;
   const double2* a1p = two ? a0p + (size_t)KB * 32 : a0p;
-  const double* cp = ym + ((size_t)d.col0 + q) * MR + g;
+  const double* cp = ym + ((size_t)it.col0 + q) * MR + g;
   double acc[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
   for (int kb0 = 0; kb0 < KB; kb0 += 8) {
     double2 a0[8], a1[8];
@@ -372,7 +377,7 @@ __global__ void __launch_bounds__(256) k_zy_multi_pk(const int2* __restrict__ it
       const int kb = kb0 + u;
       if (kb < KB) {
         const int k = kb * 8 + q;
-        const bool v0 = k < d.m, v1 = k + 4 < d.m;
+        const bool v0 = k < it.m, v1 = k + 4 < it.m;
         const double* cu = cp + (size_t)kb * 8 * MR;
         const double b00 = v0 ? __ldg(cu) : 0.0, b01 = v0 ? __ldg(cu + 8) : 0.0;
         const double b10 = v1 ? __ldg(cu + 4 * MR) : 0.0, b11 = v1 ? __ldg(cu + 4 * MR + 8) : 0.0;
@@ -389,9 +394,9 @@ __global__ void __launch_bounds__(256) k_zy_multi_pk(const int2* __restrict__ it
   }
 #pragma unroll
   for (int t = 0; t < 2; ++t) {
-    const int row = (mt0 + t) * 8 + g;
-    if ((t == 1 && !two) || row >= d.n) continue;
-    double* dst = zsm + d.idx_off + row;
+    const int row = t * 8 + g;
+    if (row >= it.rows) continue;
+    double* dst = zsm + it.dst_off + row;
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -821,7 +826,7 @@ int multi_prepare(HgPrecond* P) {
     const char* zenv = getenv("HG_Z_PACKED");
     if (!(zenv && zenv[0] == '0') && P->n_zt_items > 0) {
       std::vector<long long> zoff(P->n_cblk), toff(P->n_cblk);
-      std::vector<int2> zit;
+      std::vector<ZyItem> zit;
       long long zlen = 0, tlen = 0;
       for (int b = 0; b < P->n_cblk; ++b) {
         const CblkDesc& d = P->h_cblk[b];
@@ -831,7 +836,9 @@ int multi_prepare(HgPrecond* P) {
         zlen += MT * KB * 64;
         tlen += (long long)d.nchunk * KB * 32 * 64;
         if (d.m > 0)
-          for (int t = 0; t < (MT + 1) / 2; ++t) zit.push_back(make_int2(b, t));
+          for (int t = 0; t < (MT + 1) / 2; ++t)
+            zit.push_back(ZyItem{zoff[b] / 2 + (long long)t * 2 * KB * 32, d.idx_off + (long long)t * 16, d.col0, d.m,
+                                 std::min(16, d.n - t * 16), 0});
       }
       HG_TRY(alloc(&P->d_zypk, (size_t)std::max(zlen, 1LL)));
       HG_TRY(alloc(&P->d_ztpk, (size_t)std::max(tlen, 1LL)));
@@ -839,8 +846,8 @@ int multi_prepare(HgPrecond* P) {
       HG_CUDA_TRY(cudaMalloc(&P->d_ztpk_off, sizeof(long long) * P->n_cblk));
       HG_CUDA_TRY(cudaMemcpy(P->d_zypk_off, zoff.data(), sizeof(long long) * P->n_cblk, cudaMemcpyHostToDevice));
       HG_CUDA_TRY(cudaMemcpy(P->d_ztpk_off, toff.data(), sizeof(long long) * P->n_cblk, cudaMemcpyHostToDevice));
-      HG_CUDA_TRY(cudaMalloc(&P->d_zy_items, sizeof(int2) * std::max<size_t>(zit.size(), 1)));
-      HG_CUDA_TRY(cudaMemcpy(P->d_zy_items, zit.data(), sizeof(int2) * zit.size(), cudaMemcpyHostToDevice));
+      HG_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&P->d_zy_items), sizeof(ZyItem) * std::max<size_t>(zit.size(), 1)));
+      HG_CUDA_TRY(cudaMemcpy(P->d_zy_items, zit.data(), sizeof(ZyItem) * zit.size(), cudaMemcpyHostToDevice));
       P->n_zy_items = (int)zit.size();
       k_zpack_zy<<<dim3(64, P->n_cblk), 256>>>(P->d_cblk, P->d_zypk_off, P->d_z, reinterpret_cast<double2*>(P->d_zypk));
       HG_LAUNCH_CHECK();
