@@ -41,12 +41,16 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 }
 
 // ------------------------------------------------------------------ SpMM
+// FULL: all HG_MAX_RHS columns in their natural order (the block solve until columns converge):
+// no per-column predicates or column-list lookups, one pointer walk over the columns per nonzero
+// (the general path spends ~18 instructions per nonzero and column, this one ~6).
+template <bool FULL>
 __global__ void __launch_bounds__(256) k_spmm(int n, const int* __restrict__ ip, const int* __restrict__ ix,
                                               const double* __restrict__ a, const double* __restrict__ X,
                                               long long ldx, double* __restrict__ Y, long long ldy, ColList cols,
                                               double* __restrict__ partials, int width, int nb) {
   const int i = blockIdx.x * 256 + threadIdx.x;
-  const int nr = cols.n;
+  const int nr = FULL ? MR : cols.n;
   double s[MR];
 #pragma unroll
   for (int c = 0; c < MR; ++c) s[c] = 0.0;
@@ -55,13 +59,31 @@ __global__ void __launch_bounds__(256) k_spmm(int n, const int* __restrict__ ip,
     for (int e = ip[i]; e < e1; ++e) {
       const double av = a[e];
       const int col = ix[e];
+      if (FULL) {
+        const double* xp = X + col;
+#pragma unroll
+        for (int c = 0; c < MR; ++c) {
+          s[c] = __dadd_rn(s[c], __dmul_rn(av, __ldg(xp)));
+          xp += ldx;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < MR; ++c)
+          if (c < nr) s[c] = __dadd_rn(s[c], __dmul_rn(av, __ldg(X + (long long)cols.c[c] * ldx + col)));
+      }
+    }
+    if (FULL) {
+      double* yp = Y + i;
+#pragma unroll
+      for (int c = 0; c < MR; ++c) {
+        *yp = s[c];
+        yp += ldy;
+      }
+    } else {
 #pragma unroll
       for (int c = 0; c < MR; ++c)
-        if (c < nr) s[c] = __dadd_rn(s[c], __dmul_rn(av, __ldg(X + (long long)cols.c[c] * ldx + col)));
+        if (c < nr) Y[(long long)cols.c[c] * ldy + i] = s[c];
     }
-#pragma unroll
-    for (int c = 0; c < MR; ++c)
-      if (c < nr) Y[(long long)cols.c[c] * ldy + i] = s[c];
   }
   if (partials) {  // self dots X_c . Y_c, fixed-order block reduction per column
     __shared__ double s_w[8][MR];
@@ -100,7 +122,12 @@ static int spmm_impl(const DevCsr& A, const double* vals, const double* X, long 
     set_error("spmm: more than HG_MAX_RHS columns");
     return HG_ERR_ARG;
   }
-  k_spmm<<<nb, 256, 0, st>>>(A.n, A.indptr, A.indices, vals, X, ldx, Y, ldy, cols, partials, width, nb);
+  bool full = cols.n == MR;
+  for (int c = 0; c < MR && full; ++c) full = cols.c[c] == c;
+  if (full)
+    k_spmm<true><<<nb, 256, 0, st>>>(A.n, A.indptr, A.indices, vals, X, ldx, Y, ldy, cols, partials, width, nb);
+  else
+    k_spmm<false><<<nb, 256, 0, st>>>(A.n, A.indptr, A.indices, vals, X, ldx, Y, ldy, cols, partials, width, nb);
   HG_LAUNCH_CHECK();
   return HG_OK;
 }
@@ -865,7 +892,8 @@ int multi_prepare(HgPrecond* P) {
 
 int preload_multi() {
   cudaFuncAttributes at;
-  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_spmm));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_spmm<true>));
+  HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_spmm<false>));
   HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_zt_multi));
   HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_zy_multi));
   HG_CUDA_TRY(cudaFuncGetAttributes(&at, k_zt_multi_pk));
